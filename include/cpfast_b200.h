@@ -1,0 +1,136 @@
+/*
+ * cpfast_b200.h -- C ABI of the B200-native fast damped Gauss-Newton (fLM) CP engine.
+ *
+ * The reference (`cpfast`, pure Python/NumPy) has no FFI: its boundary is the Python API
+ *   cpfast.fit(y: DenseTensor, config: FitConfig) -> FitResult          (pkg/src/cpfast/solver.py:278-291)
+ *   cpfast.fit_complex(y, config) -> FitResult                           (pkg/src/cpfast/complexcp.py:51-54)
+ *   cpfast.solver.flm_step(y, model, mu, variant, cache, mttkrps, refine_steps)  (solver.py:189-226)
+ *   cpfast.kruskal.mttkrp(y, model, n)                                   (kruskal.py:126-135)
+ *   cpfast.kruskal.relative_error(y, model)                              (kruskal.py:163-167)
+ * This header is the native boundary those entry points are re-implemented over.  A binding is a
+ * thin ctypes / cffi / pybind layer (paper_1205_2584_b200/_native.py is the in-tree one; see
+ * INTEGRATION.md).  All pointers are plain; no torch types cross the boundary.
+ *
+ * Conventions (identical to the reference):
+ *   - tensors are column-major (mode-1 index fastest), float64 or interleaved complex128;
+ *   - factors are I_n x R column-major and are passed "stacked": the concatenation of the
+ *     column-major vectorisations of A^(1..N) (kruskal.py:70-82);
+ *   - modes are 1-based where a mode index is taken.
+ * Every call is ordered on the engine's CUDA stream; calls returning host data synchronise it.
+ * Multi-GPU: one engine per process/GPU; the tensor is slab-sharded along mode N
+ * (cpf_engine_slab) and the engines exchange MTTKRP partials with NCCL.
+ */
+#ifndef CPFAST_B200_H_
+#define CPFAST_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CPF_ABI_VERSION 1
+
+/* return codes */
+#define CPF_OK 0
+#define CPF_E_ARG (-1)         /* ValueError: bad shape / rank / variant (solver.py:72-76, kruskal.py:132-133) */
+#define CPF_E_KIND (-2)        /* TypeError / ScalarKindError (tensor.py:21-33, complexcp.py:18-22) */
+#define CPF_E_CUDA (-4)        /* CUDA runtime failure */
+#define CPF_E_NCCL (-5)        /* NCCL failure */
+#define CPF_E_ZERODIV (-6)     /* ZeroDivisionError: zero tensor / zero-norm component (solver.py:323-324, kruskal.py:184-185) */
+#define CPF_E_UNSUPPORTED (-7) /* shape outside the engine's envelope (order > 8, NR^2 too large, ...) */
+#define CPF_E_STATE (-8)       /* call out of order (no tensor / factors bound) */
+
+/* scalar kinds */
+#define CPF_REAL 0     /* float64 */
+#define CPF_COMPLEX 1  /* complex128, interleaved (re, im) */
+
+/* variants (solver.py:44 VARIANTS, LM family only) */
+#define CPF_VARIANT_AUTO 0
+#define CPF_VARIANT_FLM_A 1
+#define CPF_VARIANT_FLM_B 2
+
+/* stop codes (FitResult.stop_reason, solver.py:378-383, 349-352) */
+#define CPF_RUNNING 0
+#define CPF_STOP_TOL 1
+#define CPF_STOP_MU_OVERFLOW 2
+#define CPF_STOP_ERROR 3
+#define CPF_STOP_MAX_ITERS 4
+
+/* in-loop error codes (become "error at iteration t: <msg>", solver.py:349-352) */
+#define CPF_ERR_NONE 0
+#define CPF_ERR_SINGULAR 1         /* LinAlgError("Singular matrix") */
+#define CPF_ERR_KERNEL_SINGULAR 2  /* SingularKernelError("flm-b requested but K is singular") */
+#define CPF_ERR_PHI1_SINGULAR 3    /* SingularKernelError("I + Psi K numerically singular: Singular matrix") */
+#define CPF_ERR_ZERO_COLUMN 4      /* ZeroDivisionError while normalising an accepted candidate */
+#define CPF_ERR_NONFINITE 5
+
+typedef struct cpf_engine cpf_engine;
+
+/* IterRecord (solver.py:79-84) */
+typedef struct {
+  int32_t iter;
+  int32_t accepted;
+  double relerr;
+  double mu;
+} cpf_iter_record;
+
+typedef struct {
+  int32_t stopped;   /* CPF_RUNNING or CPF_STOP_* */
+  int32_t err_code;  /* CPF_ERR_* when stopped == CPF_STOP_ERROR */
+  int32_t err_iter;  /* iteration t of the error stop */
+  int32_t iter;      /* last completed iteration */
+  int32_t last_accepted;
+  int32_t err_column;
+  double relerr;     /* current relative error */
+  double mu;         /* current damping */
+  double ynorm;
+} cpf_status;
+
+int cpf_abi_version(void);
+int cpf_device_count(int* n);
+/* 128-byte NCCL unique id for a multi-GPU engine group (rank 0 creates, all ranks receive). */
+int cpf_nccl_unique_id(void* out128);
+
+/* Create an engine for an order-`order` tensor with global `dims`, CP rank `rank`, scalar
+ * `kind`.  world_size > 1 shards mode N across ranks and requires nccl_uid128. */
+int cpf_engine_create(cpf_engine** out, int device, int kind, int order, const int64_t* dims, int rank,
+                      int world_rank, int world_size, const void* nccl_uid128);
+void cpf_engine_destroy(cpf_engine* e);
+const char* cpf_engine_last_error(const cpf_engine* e);
+/* Local slab [lo, hi) of mode N owned by this rank. */
+int cpf_engine_slab(const cpf_engine* e, int64_t* lo, int64_t* hi);
+/* The engine's CUDA stream (cudaStream_t) for event-based timing by the caller. */
+void* cpf_engine_stream(cpf_engine* e);
+
+/* Bind the local slab (column-major, prod(dims[0:N-1]) * (hi-lo) elements).
+ * where = 0: host memory, copied (pinned or pageable); where = 1: device memory, borrowed. */
+int cpf_engine_set_tensor(cpf_engine* e, const void* data, int64_t nelem, int where);
+/* Factors, stacked (kruskal.py:70-72).  Host memory; full (replicated) factors on every rank. */
+int cpf_engine_set_factors(cpf_engine* e, const void* stacked);
+int cpf_engine_get_factors(cpf_engine* e, void* stacked);
+
+/* fit (solver.py:319-384): begin = preamble (normalise the bound factors, ||Y||, mu0, cache,
+ * MTTKRPs, initial error); step = up to n_iters LM iterations (stops early at a stop condition). */
+int cpf_engine_fit_begin(cpf_engine* e, int variant, double tau, double tol, int max_iters, cpf_status* st);
+int cpf_engine_fit_step(cpf_engine* e, int n_iters, cpf_status* st);
+int cpf_engine_trace(cpf_engine* e, cpf_iter_record* out, int cap, int* n);
+
+/* Building blocks at the bound factors, no normalisation (kruskal.py / solver.py semantics). */
+int cpf_engine_mttkrp(cpf_engine* e, int mode, void* out);            /* mode 1..N; 0 = all, stacked */
+int cpf_engine_relative_error(cpf_engine* e, double* out);            /* ||Y-X||/||Y|| */
+int cpf_engine_flm_step(cpf_engine* e, double mu, int variant, int refine_steps, void* cand_stacked,
+                        int* err_code);
+
+/* Per-phase device time accumulated with CUDA events on the engine stream (profiling on/off).
+ * Phases: 0 pass A, 1 pass B, 2 LU factor, 3 solves, 4 other; counts = launches per phase. */
+int cpf_engine_profile(cpf_engine* e, int enable);
+int cpf_engine_phase_times(cpf_engine* e, double* ms_out, int64_t* counts_out, int nphases);
+/* Number of kernels this engine has launched (for the bench's gpu_launches count). */
+int64_t cpf_engine_launch_count(const cpf_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPFAST_B200_H_ */

@@ -1,0 +1,34 @@
+"""B200-native fast damped Gauss-Newton (fLM) CP decomposition -- drop-in for ``cpfast``'s solver path.
+
+Public surface mirrors the reference package (cpfast/__init__.py:32-33 and the solver module):
+``fit``, ``fit_complex``, ``FitConfig``, ``FitResult``, ``IterRecord``, ``flm_step``, ``mttkrp``,
+``relative_error``, ``DenseTensor``, ``KruskalModel``.  All numerics run in the sm_100a engine
+(``_lib/libcpfast_b200.so``, C ABI in ``include/cpfast_b200.h``).
+"""
+
+from .tensor import COMPLEX, REAL, DenseTensor, KruskalModel, ScalarKindError, model_from_vector
+from .solver import (
+    LM_VARIANTS,
+    MU_OVERFLOW,
+    VARIANTS,
+    FitConfig,
+    FitResult,
+    IterRecord,
+    SingularKernelError,
+    fit,
+    fit_complex,
+    flm_step,
+    mttkrp,
+    random_init,
+    relative_error,
+    slab_bounds,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "COMPLEX", "REAL", "DenseTensor", "KruskalModel", "ScalarKindError", "model_from_vector",
+    "LM_VARIANTS", "MU_OVERFLOW", "VARIANTS", "FitConfig", "FitResult", "IterRecord",
+    "SingularKernelError", "fit", "fit_complex", "flm_step", "mttkrp", "random_init",
+    "relative_error", "slab_bounds",
+]

@@ -1,0 +1,993 @@
+// B200 fLM CP engine: host orchestration of one fit behind the C ABI in include/cpfast_b200.h.
+//
+// One engine = one GPU = one process.  It owns every device buffer of the fit; the LM control
+// state (mu, growth, err, accept/stop flags, the 10-delta tolerance window, the trace) lives on
+// the device (LmDeviceState), so an iteration is a fixed launch sequence and the host only polls
+// the state once per iteration (or per batch).  Reference semantics: cpfast/solver.py:319-384.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cpfast_b200.h"
+
+struct CudaError : std::runtime_error {
+  CudaError(cudaError_t e, const char* expr, const char* file, int line)
+      : std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " at " + file + ":" +
+                           std::to_string(line) + " (" + expr + ")") {}
+};
+struct ApiError : std::runtime_error {
+  int code;
+  ApiError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#include "cpf_common.cuh"
+#include "lu.cuh"
+#include "phi.cuh"
+#include "small_ops.cuh"
+#include "tensor_pass.cuh"
+
+#define NCCL_CHECK(expr)                                                                   \
+  do {                                                                                     \
+    ncclResult_t _r = (expr);                                                              \
+    if (_r != ncclSuccess) throw ApiError(CPF_E_NCCL, std::string("NCCL error ") + ncclGetErrorString(_r) + " (" #expr ")"); \
+  } while (0)
+
+namespace cpf {
+
+static int padded_rank(int R) {
+  static const int table[] = {1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 16, 20, 24, 32, 40, 48, 64};
+  for (int v : table)
+    if (v >= R) return v;
+  return -1;
+}
+
+enum Phase { kPhPassA = 0, kPhPassB = 1, kPhLU = 2, kPhSolve = 3, kPhOther = 4, kNumPhases = 5 };
+
+// ------------------------------------------------------------------------------------------
+struct EngineBase {
+  virtual ~EngineBase() = default;
+  std::string last_error;
+  virtual void slab(int64_t* lo, int64_t* hi) const = 0;
+  virtual void* stream() = 0;
+  virtual void set_tensor(const void* p, int64_t n, int where) = 0;
+  virtual void set_factors(const void* p) = 0;
+  virtual void get_factors(void* p) = 0;
+  virtual void fit_begin(int variant, double tau, double tol, int max_iters, cpf_status* st) = 0;
+  virtual void fit_step(int n, cpf_status* st) = 0;
+  virtual int trace(cpf_iter_record* out, int cap) = 0;
+  virtual void mttkrp(int mode, void* out) = 0;
+  virtual double relative_error() = 0;
+  virtual int flm_step(double mu, int variant, int refine, void* out) = 0;
+  virtual void profile(int on) = 0;
+  virtual void phase_times(double* ms, int64_t* cnt, int n) = 0;
+  virtual int64_t launches() const = 0;
+};
+
+template <class T>
+struct Engine final : EngineBase {
+  // ---- geometry
+  int dev = 0, N = 0, R = 0, RP = 0, world = 1, wrank = 0;
+  int64_t dims[kMaxModes] = {0};
+  int64_t offs[kMaxModes] = {0};
+  int64_t Tsum = 0, RT = 0;
+  int64_t I1 = 0, Lmid = 1, Lrows = 0, IN = 0, slab_lo = 0, slab_hi = 0, Cloc = 0, Cpad = 0, Jloc = 0;
+  int nB = 0;
+  Modes md{};
+  MidGeom mg{};
+  cudaStream_t s = nullptr;
+  ncclComm_t comm = nullptr;
+  int64_t nlaunch = 0;
+
+  // ---- tensor
+  const T* Y = nullptr;
+  T* Yown = nullptr;
+  bool have_tensor = false, have_factors = false;
+
+  // ---- device buffers
+  T *A = nullptr, *Ac = nullptr, *M = nullptr, *Mc = nullptr, *D = nullptr, *G = nullptr, *Cand = nullptr;
+  T *V1 = nullptr, *V2 = nullptr, *V3 = nullptr, *V4 = nullptr;
+  T *Cg = nullptr, *Ccg = nullptr, *Gx = nullptr, *Gp = nullptr, *Gf = nullptr, *Gti = nullptr, *Gi = nullptr;
+  T *W1 = nullptr, *Sm = nullptr;
+  T *wvec = nullptr, *fvec = nullptr, *xvec = nullptr, *Phi = nullptr;
+  T *A1c = nullptr, *KMc = nullptr, *WNc = nullptr, *zpart = nullptr, *m1part = nullptr, *bpart = nullptr;
+  T *pa_out = nullptr, *pb_out = nullptr, *pb_all = nullptr;
+  double *norms = nullptr, *dscal = nullptr, *red = nullptr;
+  int* ibuf = nullptr;
+  LuWork lu{};
+  LmDeviceState* st = nullptr;
+  DevFlags* fl = nullptr;
+  IterRecordDev* dtrace = nullptr;
+  int* kinv_ok = nullptr;
+  LmDeviceState* hst = nullptr;  // pinned mirror
+  int trace_cap = 0;
+  int epoch = 0;
+
+  // pass-A / pass-B launch geometry
+  int pa_threads = 256, pa_TI = 1, pa_TM = 1, pa_tiles = 1, pa_groups = 1;
+  int64_t pa_mper = 1;
+  size_t pa_smem = 0;
+  int pb_threads = 256, pb_TI = 1, pb_TM = 1, pb_tiles = 1, pb_chunks = 1;
+  int64_t pb_mper = 1;
+  int lu_kb = 32, lu_cl = 1, lu_rpc = 0;
+  size_t lu_smem = 0;
+
+  // profiling
+  bool prof = false;
+  struct Ev { int ph; cudaEvent_t a, b; };
+  std::vector<Ev> evs;
+  double ph_ms[kNumPhases] = {0};
+  int64_t ph_cnt[kNumPhases] = {0};
+
+  // ------------------------------------------------------------------------------------------
+  Engine(int device, int order, const int64_t* d, int rank, int wr, int ws, const void* uid) {
+    if (order < 2 || order > kMaxModes) throw ApiError(CPF_E_UNSUPPORTED, "order must be in [2, 8]");
+    if (rank < 1) throw ApiError(CPF_E_ARG, "rank must be >= 1");
+    RP = padded_rank(rank);
+    if (RP < 0) throw ApiError(CPF_E_UNSUPPORTED, "rank > 64 is outside the engine envelope");
+    dev = device;
+    N = order;
+    R = rank;
+    world = ws;
+    wrank = wr;
+    CPF_CUDA_CHECK(cudaSetDevice(dev));
+    CPF_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (int n = 0; n < N; ++n) {
+      if (d[n] < 1) throw ApiError(CPF_E_ARG, "dims must be >= 1");
+      dims[n] = d[n];
+      offs[n] = (int64_t)R * Tsum;
+      Tsum += d[n];
+    }
+    RT = (int64_t)R * Tsum;
+    md.N = N;
+    md.R = R;
+    for (int n = 0; n < N; ++n) { md.dims[n] = dims[n]; md.offs[n] = offs[n]; }
+    I1 = dims[0];
+    Lmid = 1;
+    for (int n = 1; n < N - 1; ++n) Lmid *= dims[n];
+    Lrows = I1 * Lmid;
+    IN = dims[N - 1];
+    mg.nmid = N - 2;
+    for (int k = 0; k < N - 2; ++k) { mg.dims[k] = dims[k + 1]; mg.offs[k] = offs[k + 1]; }
+    // slab sharding along mode N: ceil(IN / world) per rank
+    const int64_t per = (IN + world - 1) / world;
+    slab_lo = std::min<int64_t>(IN, per * wrank);
+    slab_hi = std::min<int64_t>(IN, slab_lo + per);
+    Cloc = slab_hi - slab_lo;
+    Cpad = per;
+    Jloc = Lrows * Cloc;
+    nB = N * R * R;
+    if ((int64_t)nB * nB > (int64_t)1 << 31) throw ApiError(CPF_E_UNSUPPORTED, "N*R^2 too large");
+    if (world > 1) {
+      if (!uid) throw ApiError(CPF_E_ARG, "world_size > 1 needs an NCCL unique id");
+      ncclUniqueId id;
+      std::memcpy(&id, uid, sizeof(id));
+      NCCL_CHECK(ncclCommInitRank(&comm, world, id, wrank));
+    }
+    alloc();
+    plan();
+  }
+
+  ~Engine() override {
+    cudaSetDevice(dev);
+    if (s) cudaStreamSynchronize(s);
+    for (auto& e : evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    void* ptrs[] = {Yown, A, Ac, M, Mc, D, G, Cand, V1, V2, V3, V4, Cg, Ccg, Gx, Gp, Gf, Gti, Gi, W1, Sm,
+                    wvec, fvec, xvec, Phi, A1c, KMc, WNc, zpart, m1part, bpart, pa_out, pb_out, pb_all,
+                    norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    if (hst) cudaFreeHost(hst);
+    if (comm) ncclCommDestroy(comm);
+    if (s) cudaStreamDestroy(s);
+  }
+
+  template <class U>
+  U* dalloc(size_t n) {
+    void* p = nullptr;
+    CPF_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(U)));
+    CPF_CUDA_CHECK(cudaMemsetAsync(p, 0, std::max<size_t>(n, 1) * sizeof(U), s));
+    return static_cast<U*>(p);
+  }
+
+  void alloc() {
+    const size_t R2 = (size_t)R * R;
+    A = dalloc<T>(RT); Ac = dalloc<T>(RT); M = dalloc<T>(RT); Mc = dalloc<T>(RT); D = dalloc<T>(RT);
+    G = dalloc<T>(RT); Cand = dalloc<T>(RT);
+    V1 = dalloc<T>(RT); V2 = dalloc<T>(RT); V3 = dalloc<T>(RT); V4 = dalloc<T>(RT);
+    Cg = dalloc<T>(N * R2); Ccg = dalloc<T>(N * R2); Gx = dalloc<T>(N * R2); Gp = dalloc<T>((size_t)N * N * R2);
+    Gf = dalloc<T>(R2); Gti = dalloc<T>(N * R2); Gi = dalloc<T>(N * R2); W1 = dalloc<T>(N * R2); Sm = dalloc<T>(N * R2);
+    wvec = dalloc<T>(nB); fvec = dalloc<T>(nB); xvec = dalloc<T>(nB);
+    Phi = dalloc<T>((size_t)nB * nB);
+    A1c = dalloc<T>((size_t)I1 * RP);
+    KMc = dalloc<T>((size_t)Lmid * RP);
+    WNc = dalloc<T>((size_t)std::max<int64_t>(Cloc, 1) * RP);
+    pa_out = dalloc<T>((size_t)(I1 + Lmid) * R);
+    pb_out = dalloc<T>((size_t)Cpad * R);
+    pb_all = dalloc<T>((size_t)Cpad * R * world);
+    norms = dalloc<double>((size_t)N * R);
+    dscal = dalloc<double>(16);
+    red = dalloc<double>(4096);
+    const int nblk32 = (nB + 31) / 32;
+    ibuf = dalloc<int>((size_t)2 * nB + 4 * kLuMaxKB + 8 + nblk32);
+    lu.perm = ibuf;
+    lu.ipiv = ibuf + nB;
+    lu.gather = ibuf + 2 * nB;
+    lu.gcount = lu.gather + 4 * kLuMaxKB;
+    lu.info = lu.gcount + 1;
+    lu.ticket = lu.info + 1;
+    lu.ready = lu.ticket + 4;
+    st = dalloc<LmDeviceState>(1);
+    fl = dalloc<DevFlags>(1);
+    kinv_ok = dalloc<int>(1);
+    CPF_CUDA_CHECK(cudaMallocHost(&hst, sizeof(LmDeviceState)));
+    std::memset(hst, 0, sizeof(LmDeviceState));
+  }
+
+  // Launch geometry for the tensor passes and the LU panel.
+  void plan() {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const size_t es = sizeof(T);
+    // pass A: threads sized so 2*threads*RP*es (+W stage) fits ~160 KB
+    pa_threads = 256;
+    while (pa_threads > 32 && (2 * (size_t)pa_threads * RP + kPassCK * RP) * es > 160 * 1024) pa_threads /= 2;
+    pa_TI = (int)std::min<int64_t>(I1, pa_threads);
+    pa_TM = pa_threads / pa_TI;
+    pa_tiles = (int)((I1 + pa_TI - 1) / pa_TI);
+    const int64_t target = (int64_t)nsm * 4;
+    int64_t groups = std::max<int64_t>(1, target / pa_tiles);
+    groups = std::min<int64_t>(groups, (Lmid + pa_TM - 1) / pa_TM);
+    pa_mper = (Lmid + groups - 1) / groups;
+    pa_mper = ((pa_mper + pa_TM - 1) / pa_TM) * pa_TM;
+    pa_groups = (int)((Lmid + pa_mper - 1) / pa_mper);
+    pa_smem = (2 * (size_t)pa_threads * RP + kPassCK * RP) * es;
+    zpart = dalloc<T>((size_t)pa_tiles * Lmid * RP);
+    m1part = dalloc<T>((size_t)pa_groups * I1 * RP);
+    // pass B
+    pb_threads = 256;
+    pb_TI = (int)std::min<int64_t>(I1, pb_threads);
+    pb_TM = pb_threads / pb_TI;
+    pb_tiles = (int)((I1 + pb_TI - 1) / pb_TI);
+    int64_t per_c = std::max<int64_t>(1, target / std::max<int64_t>(1, Cloc * pb_tiles));
+    per_c = std::min<int64_t>(per_c, (Lmid + pb_TM - 1) / pb_TM);
+    pb_mper = (Lmid + per_c - 1) / per_c;
+    pb_chunks = (int)((Lmid + pb_mper - 1) / pb_mper);
+    bpart = dalloc<T>((size_t)std::max<int64_t>(Cloc, 1) * pb_chunks * pb_tiles * RP);
+    // LU panel: smallest cluster whose smem holds the (full-height) first panel
+    lu_kb = std::min(kLuMaxKB, nB);
+    const size_t cap = 200 * 1024;
+    for (;;) {
+      bool ok = false;
+      for (int cl = 1; cl <= kLuMaxCluster; cl *= 2) {
+        int rpc = (nB + cl - 1) / cl;
+        if (panel_smem_bytes<T>(rpc, lu_kb, cl) <= cap) { lu_cl = cl; lu_rpc = rpc; ok = true; break; }
+      }
+      if (ok) break;
+      if (lu_kb <= 4) throw ApiError(CPF_E_UNSUPPORTED, "N*R^2 too large for the LU panel");
+      lu_kb /= 2;
+    }
+    lu_smem = panel_smem_bytes<T>(lu_rpc, lu_kb, lu_cl);
+    CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lu_smem));
+    if (lu_cl > 8) CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    set_pass_attrs();
+    CPF_CUDA_CHECK(cudaFuncSetAttribute(k_damped_inverses<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(2 * R * R * sizeof(T))));
+  }
+
+  // ------------------------------------------------------------------------------------------
+  // launch helpers
+  template <class K, class... Args>
+  void launch(K kern, dim3 g, dim3 b, size_t smem, Args... args) {
+    if (g.x == 0 || g.y == 0 || g.z == 0) return;
+    kern<<<g, b, smem, s>>>(args...);
+    ++nlaunch;
+    CPF_CUDA_CHECK(cudaGetLastError());
+  }
+  static unsigned nblocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+  int cur_phase = -1;
+  cudaEvent_t cur_ev = nullptr;
+  void ph_begin(int ph) {
+    if (!prof) return;
+    cudaEvent_t a;
+    CPF_CUDA_CHECK(cudaEventCreate(&a));
+    CPF_CUDA_CHECK(cudaEventRecord(a, s));
+    cur_phase = ph;
+    cur_ev = a;
+  }
+  void ph_end() {
+    if (!prof || cur_phase < 0) return;
+    cudaEvent_t b;
+    CPF_CUDA_CHECK(cudaEventCreate(&b));
+    CPF_CUDA_CHECK(cudaEventRecord(b, s));
+    evs.push_back({cur_phase, cur_ev, b});
+    cur_phase = -1;
+  }
+
+  // ------------------------------------------------------------------------------------------
+  // tensor passes
+  // ------------------------------------------------------------------------------------------
+  template <int RPc>
+  void set_pass_attrs_t() {
+    CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_a<T, RPc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pa_smem));
+  }
+  void set_pass_attrs() { dispatch_rp([&](auto rpc) { this->template set_pass_attrs_t<decltype(rpc)::value>(); }); }
+
+  template <int V> struct IC { static constexpr int value = V; };
+  template <class F>
+  void dispatch_rp(F&& f) {
+    switch (RP) {
+      case 1: f(IC<1>{}); break;
+      case 2: f(IC<2>{}); break;
+      case 3: f(IC<3>{}); break;
+      case 4: f(IC<4>{}); break;
+      case 5: f(IC<5>{}); break;
+      case 6: f(IC<6>{}); break;
+      case 7: f(IC<7>{}); break;
+      case 8: f(IC<8>{}); break;
+      case 10: f(IC<10>{}); break;
+      case 12: f(IC<12>{}); break;
+      case 16: f(IC<16>{}); break;
+      case 20: f(IC<20>{}); break;
+      case 24: f(IC<24>{}); break;
+      case 32: f(IC<32>{}); break;
+      case 40: f(IC<40>{}); break;
+      case 48: f(IC<48>{}); break;
+      case 64: f(IC<64>{}); break;
+      default: throw ApiError(CPF_E_UNSUPPORTED, "unsupported padded rank");
+    }
+  }
+
+  // conj row-major operand copies for factors F (stacked)
+  void prep_operands(const T* F, bool need_wn, int gate) {
+    launch(k_conj_rowmajor<T>, nblocks(I1 * RP, 256), 256, 0, F + offs[0], I1, (int64_t)0, I1, R, RP, A1c, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    if (N == 3) {
+      launch(k_conj_rowmajor<T>, nblocks(Lmid * RP, 256), 256, 0, F + offs[1], Lmid, (int64_t)0, Lmid, R, RP, KMc, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    } else {
+      launch(k_krmid<T>, nblocks(Lmid * RP, 256), 256, 0, (const T*)F, mg, Lmid, R, RP, KMc, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    }
+    if (need_wn && Cloc > 0)
+      launch(k_conj_rowmajor<T>, nblocks(Cloc * RP, 256), 256, 0, F + offs[N - 1], Cloc, slab_lo, IN, R, RP, WNc, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+  }
+
+  // Pass A at factors F -> out modes 1..N-1 of Mout (stacked), allreduced.
+  void pass_a(const T* F, T* Mout, int gate) {
+    prep_operands(F, true, gate);
+    ph_begin(kPhPassA);
+    if (Cloc > 0) {
+      dispatch_rp([&](auto rpc) {
+        constexpr int RPc = decltype(rpc)::value;
+        launch(k_pass_a<T, RPc>, dim3(pa_tiles, pa_groups), dim3(pa_threads), pa_smem, Y, I1, Lmid, Cloc,
+               (const T*)WNc, (const T*)A1c, (const T*)KMc, pa_TI, pa_TM, pa_mper, zpart, m1part, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+      });
+      launch(k_pass_a_reduce<T>, nblocks((I1 + Lmid) * R, 256), 256, 0, (const T*)m1part, pa_groups,
+             (const T*)zpart, pa_tiles, I1, Lmid, R, RP, pa_out, pa_out + I1 * R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    } else {
+      CPF_CUDA_CHECK(cudaMemsetAsync(pa_out, 0, sizeof(T) * (I1 + Lmid) * R, s));
+    }
+    ph_end();
+    if (world > 1) {
+      NCCL_CHECK(ncclAllReduce(pa_out, pa_out, (size_t)(I1 + Lmid) * R * (sizeof(T) / sizeof(double)), ncclDouble,
+                               ncclSum, comm, s));
+    }
+    // scatter: M_1 = pa_out[0 : I1 R]; N==3: M_2 = Z; N>=4: M_2..M_{N-1} from Z (at F)
+    launch(k_copy<T>, nblocks(I1 * R, 256), 256, 0, (const T*)pa_out, Mout + offs[0], I1 * R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    if (N == 3) {
+      launch(k_copy<T>, nblocks(Lmid * R, 256), 256, 0, (const T*)(pa_out + I1 * R), Mout + offs[1], Lmid * R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    } else if (N >= 4) {
+      for (int k = 0; k < N - 2; ++k)
+        launch(k_mid_mttkrp<T>, nblocks(mg.dims[k] * R, 128), 128, 0, (const T*)(pa_out + I1 * R), Lmid, F, mg, k, R,
+               Mout + offs[k + 1], (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    }
+  }
+
+  // Pass B at factors F -> mode N of Mout (allgathered).
+  void pass_b(const T* F, T* Mout, int gate) {
+    prep_operands(F, false, gate);
+    ph_begin(kPhPassB);
+    if (Cloc > 0) {
+      dispatch_rp([&](auto rpc) {
+        constexpr int RPc = decltype(rpc)::value;
+        const size_t smem = sizeof(T) * RPc * ((pb_threads + 31) / 32);
+        launch(k_pass_b<T, RPc>, dim3((unsigned)Cloc, pb_chunks, pb_tiles), dim3(pb_threads), smem, Y, I1, Lmid,
+               Cloc, (const T*)A1c, (const T*)KMc, pb_TI, pb_TM, pb_mper, bpart, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+      });
+    }
+    ph_end();
+    if (world == 1) {
+      launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, (const T*)bpart, Cloc, pb_chunks * pb_tiles, R, RP,
+             IN, Mout + offs[N - 1], (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    } else {
+      CPF_CUDA_CHECK(cudaMemsetAsync(pb_out, 0, sizeof(T) * Cpad * R, s));
+      if (Cloc > 0)
+        launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, (const T*)bpart, Cloc, pb_chunks * pb_tiles, R, RP,
+               Cpad, pb_out, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+      const size_t cnt = (size_t)Cpad * R * (sizeof(T) / sizeof(double));
+      NCCL_CHECK(ncclAllGather(pb_out, pb_all, cnt, ncclDouble, comm, s));
+      // pb_all[rank][c + Cpad r] -> Mout_N[(rank*Cpad + c) + IN r]
+      for (int q = 0; q < world; ++q) {
+        const int64_t lo = std::min<int64_t>(IN, (int64_t)q * Cpad);
+        const int64_t cnt_rows = std::min<int64_t>(IN, lo + Cpad) - lo;
+        if (cnt_rows <= 0) continue;
+        launch(k_copy2d<T>, nblocks(cnt_rows * R, 256), 256, 0, (const T*)(pb_all + (size_t)q * Cpad * R), Cpad,
+               Mout + offs[N - 1] + lo, IN, cnt_rows, (int64_t)R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+      }
+    }
+  }
+
+  // ------------------------------------------------------------------------------------------
+  // building blocks
+  // ------------------------------------------------------------------------------------------
+  void cross_gram(const T* X, const T* Yv, T* out, int gate) {
+    launch(k_cross_gram<T>, dim3(R * R, N), 128, 0, X, Yv, md, out, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+  }
+  void cache_from_grams(const T* C, int gate) {
+    launch(k_hadamards<T>, nblocks(R * R, 128), 128, 0, C, N, R, Gx, Gp, Gf, (const LmDeviceState*)st,
+           (const DevFlags*)fl, gate);
+    launch(k_kernel_flag<T>, 1, 256, 0, (const T*)Gp, N, R, st, (const DevFlags*)fl, gate, kinv_ok);
+  }
+  void tall(const TallArgs& a, int gate) {
+    int64_t maxrows = 0;
+    for (int n = 0; n < N; ++n) maxrows = std::max(maxrows, dims[n] * R);
+    launch(k_tall<T>, dim3(nblocks(maxrows, 128), N), 128, 2 * R * R * sizeof(T), a, md, (const LmDeviceState*)st,
+           (const DevFlags*)fl, gate);
+  }
+  void axpby(const T* x, double al, const T* y, double be, T* out, int gate) {
+    launch(k_axpby<T>, nblocks(RT, 256), 256, 0, x, al, y, be, out, RT, (const LmDeviceState*)st, (const DevFlags*)fl,
+           gate);
+  }
+  void small(int op, const T* P0, const T* P1, T* out, int gate) {
+    launch(k_small<T>, N, 128, 2 * R * R * sizeof(T), op, P0, P1, (const T*)Gx, (const T*)Gti, (const T*)Gp, N, R, out,
+           (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+  }
+  // gradient G = M - A Gamma^T (solver.py:251-256)
+  void gradient(int gate) {
+    TallArgs a{};
+    a.X1 = A; a.S1 = Gx; a.t1 = 1; a.s1stride = (int64_t)R * R;
+    a.X4 = M; a.coef4 = 1.0; a.neg1 = 1;
+    a.out = G;
+    tall(a, gate);
+  }
+  void normalize(const T* X, T* out, int gate, int mode) {
+    launch(k_colnorms<T>, dim3(R, N), 256, 0, X, md, norms, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    launch(k_normalize<T>, R, 256, 0, X, md, (const double*)norms, out, st, (const DevFlags*)fl, gate, mode);
+  }
+
+  // ---- LU of Phi and the B-application
+  void lu_factor(int gate_running) {
+    ph_begin(kPhLU);
+    launch(k_lu_init, nblocks(nB, 256), 256, 0, lu.perm, nB, lu.info);
+    for (int k0 = 0; k0 < nB; k0 += lu_kb) {
+      const int kb = std::min(lu_kb, nB - k0);
+      const int m = nB - k0;
+      int cl = lu_cl;
+      while (cl > 1 && (m + cl - 1) / cl < 1) cl /= 2;
+      const int rpc = (m + cl - 1) / cl;
+      {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(cl);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = panel_smem_bytes<T>(rpc, kb, cl);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_panel_lu<T>, Phi, nB, nB, k0, kb, rpc, lu,
+                                          (const LmDeviceState*)st, gate_running));
+        ++nlaunch;
+      }
+      {
+        // always launched: block 0 also composes the panel interchange into perm
+        const int cb = 256 / (2 * kLuMaxKB);
+        const int ncols = nB - kb;
+        launch(k_row_gather<T>, std::max(1u, nblocks(ncols, cb)), 256, 256 * sizeof(T), Phi, nB, nB, k0, kb, lu,
+               (const LmDeviceState*)st, gate_running);
+      }
+      const int rest = nB - k0 - kb;
+      if (rest > 0) {
+        launch(k_trsm_llnu<T, kLuMaxKB>, nblocks(rest, 64), 64, 0, Phi, nB, nB, k0, kb, (const LmDeviceState*)st,
+               gate_running);
+        launch(k_gemm_sub<T>, dim3(nblocks(rest, 64), nblocks(rest, 64)), 256, 0, Phi, nB, k0 + kb, k0 + kb, k0, rest,
+               rest, kb, (const LmDeviceState*)st, gate_running);
+      }
+    }
+    launch(k_lu_info_to_err, 1, 1, 0, (const int*)lu.info, st);
+    ph_end();
+  }
+  // f = B w  (flm-b: Phi^{-1} w; flm-a: K Phi^{-1} w)
+  void apply_b(const T* w, T* f, int gate_running) {
+    ph_begin(kPhSolve);
+    launch(k_perm_gather<T>, nblocks(nB, 256), 256, 0, w, (const int*)lu.perm, nB, xvec, (const LmDeviceState*)st,
+           gate_running);
+    const int nblk = (nB + 31) / 32;
+    ++epoch;
+    CPF_CUDA_CHECK(cudaMemsetAsync(lu.ticket, 0, sizeof(int) * 2, s));
+    launch(k_trsv<T, true>, nblk, 128, 0, (const T*)Phi, nB, nB, xvec, lu.ticket, lu.ready, epoch,
+           (const LmDeviceState*)st, gate_running);
+    ++epoch;
+    launch(k_trsv<T, false>, nblk, 128, 0, (const T*)Phi, nB, nB, xvec, lu.ticket + 1, lu.ready, epoch,
+           (const LmDeviceState*)st, gate_running);
+    launch(k_apply_k<T>, nblocks(nB, 256), 256, 0, (const T*)xvec, N, R, (const T*)Gp, f, (const LmDeviceState*)st,
+           gate_running);
+    ph_end();
+  }
+
+  // fLM candidate at (A, cache, M, G) with the state's mu -> Cand  (solver.py:189-226)
+  void candidate(int refine_steps, int gate) {
+    const int gr = gate == kRunning ? 1 : 0;
+    launch(k_damped_inverses<T>, 2 * N, 128, 2 * R * R * sizeof(T), (const T*)Gx, N, R, Gti, Gi, st,
+           (const DevFlags*)fl, gate, (const int*)kinv_ok, (const double*)nullptr);
+    // damped factors D = M Gti
+    { TallArgs a{}; a.X1 = M; a.S1 = Gti; a.s1stride = (int64_t)R * R; a.out = D; tall(a, gate); }
+    // w = vec(A^H D - C Gamma^T Gti)
+    cross_gram(A, D, W1, gate);
+    small(kOpW, W1, Cg, wvec, gate);
+    // core system
+    launch(k_phi_assemble<T>, nblocks((int64_t)nB * nB, 256), 256, 0, Phi, N, R, (const T*)Cg, (const T*)Gi,
+           (const T*)Gp, (const T*)Gf, (const LmDeviceState*)st, gr);
+    lu_factor(gr);
+    apply_b(wvec, fvec, gr);
+    // update: Cand = D + A (I - (F + Gamma^T) Gti)
+    small(kOpE, fvec, nullptr, Sm, gate);
+    { TallArgs a{}; a.X1 = A; a.S1 = Sm; a.s1stride = (int64_t)R * R; a.X4 = D; a.coef4 = 1.0; a.out = Cand; tall(a, gate); }
+    if (refine_steps > 0) {
+      axpby(Cand, 1.0, A, -1.0, V1, gate);  // delta
+      for (int it = 0; it < refine_steps; ++it) {
+        // (H + mu I) delta  (hessian.py:311-326)
+        cross_gram(A, V1, W1, gate);
+        small(kOpS, W1, nullptr, Sm, gate);
+        {
+          TallArgs a{};
+          a.X1 = V1; a.S1 = Gx; a.t1 = 1; a.s1stride = (int64_t)R * R;
+          a.X3 = V1; a.coef3_mu = 1;
+          a.X2 = A; a.S2 = Sm; a.s2stride = (int64_t)R * R;
+          a.out = V2;
+          tall(a, gate);
+        }
+        axpby(G, 1.0, V2, -1.0, V3, gate);  // resid = g - Hd
+        // (H + mu I)^{-1} resid  (hessian.py:329-348)
+        { TallArgs a{}; a.X1 = V3; a.S1 = Gti; a.s1stride = (int64_t)R * R; a.out = V4; tall(a, gate); }
+        cross_gram(A, V4, wvec, gate);
+        apply_b(wvec, fvec, gr);
+        small(kOpYG, fvec, nullptr, Sm, gate);
+        { TallArgs a{}; a.X1 = A; a.S1 = Sm; a.s1stride = (int64_t)R * R; a.neg1 = 1; a.X4 = V4; a.coef4 = 1.0; a.out = V2; tall(a, gate); }
+        axpby(V1, 1.0, V2, 1.0, V1, gate);  // delta += ...
+      }
+      axpby(A, 1.0, V1, 1.0, Cand, gate);  // model_from_vector(base + delta)
+    }
+  }
+
+  // cache (Grams, Hadamards, K flag), MTTKRPs and gradient at the current factors A
+  void build_cache_and_mttkrps(int gate) {
+    cross_gram(A, A, Cg, gate);
+    cache_from_grams(Cg, gate);
+    pass_a(A, M, gate);
+    pass_b(A, M, gate);
+    gradient(gate);
+  }
+
+  double host_yx_from(const T* Mx, const T* F) {
+    launch(k_redot<T>, 1, 1024, 0, F + offs[0], Mx + offs[0], I1 * R, 0, dscal + 0, (const LmDeviceState*)st,
+           (const DevFlags*)fl, (int)kAlways);
+    double v;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(&v, dscal + 0, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    return v;
+  }
+
+  double ynorm_sq() {
+    const int nb = 1024;
+    if (Jloc > 0) {
+      launch(k_sumsq_partial<T>, nb, 256, 0, Y, Jloc, red);
+      launch(k_sum_partials, 1, 1024, 0, (const double*)red, nb, dscal + 1);
+    } else {
+      CPF_CUDA_CHECK(cudaMemsetAsync(dscal + 1, 0, sizeof(double), s));
+    }
+    if (world > 1) NCCL_CHECK(ncclAllReduce(dscal + 1, dscal + 1, 1, ncclDouble, ncclSum, comm, s));
+    double v;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(&v, dscal + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    return v;
+  }
+
+  void require_ready() {
+    if (!have_tensor) throw ApiError(CPF_E_STATE, "no tensor bound");
+    if (!have_factors) throw ApiError(CPF_E_STATE, "no factors bound");
+  }
+
+  void reset_state(int variant, double mu, double tol, int max_iters) {
+    std::memset(hst, 0, sizeof(LmDeviceState));
+    hst->mu = mu;
+    hst->growth = 2.0;
+    hst->variant = variant;
+    hst->tol = tol;
+    hst->max_iters = max_iters;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(st, hst, sizeof(LmDeviceState), cudaMemcpyHostToDevice, s));
+    CPF_CUDA_CHECK(cudaMemsetAsync(fl, 0, sizeof(DevFlags), s));
+  }
+  void pull_state() {
+    CPF_CUDA_CHECK(cudaMemcpyAsync(hst, st, sizeof(LmDeviceState), cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  void fill_status(cpf_status* o) {
+    if (!o) return;
+    o->stopped = hst->stopped;
+    o->err_code = hst->err_code;
+    o->err_iter = hst->err_iter;
+    o->iter = hst->iter;
+    o->last_accepted = hst->accepted;
+    o->err_column = 0;
+    o->relerr = hst->err;
+    o->mu = hst->mu;
+    o->ynorm = hst->ynorm;
+  }
+
+  // ------------------------------------------------------------------------------------------
+  // EngineBase
+  // ------------------------------------------------------------------------------------------
+  void slab(int64_t* lo, int64_t* hi) const override { *lo = slab_lo; *hi = slab_hi; }
+  void* stream() override { return (void*)s; }
+
+  void set_tensor(const void* p, int64_t n, int where) override {
+    if (n != Jloc) throw ApiError(CPF_E_ARG, "tensor slab size mismatch: expected " + std::to_string(Jloc));
+    CPF_CUDA_CHECK(cudaSetDevice(dev));
+    if (where == 1) {
+      if (Yown) { CPF_CUDA_CHECK(cudaFree(Yown)); Yown = nullptr; }
+      Y = static_cast<const T*>(p);
+    } else {
+      if (!Yown) {
+        void* q = nullptr;
+        CPF_CUDA_CHECK(cudaMalloc(&q, std::max<int64_t>(Jloc, 1) * sizeof(T)));
+        Yown = static_cast<T*>(q);
+      }
+      if (Jloc > 0) CPF_CUDA_CHECK(cudaMemcpyAsync(Yown, p, Jloc * sizeof(T), cudaMemcpyHostToDevice, s));
+      Y = Yown;
+    }
+    have_tensor = true;
+  }
+  void set_factors(const void* p) override {
+    CPF_CUDA_CHECK(cudaMemcpyAsync(A, p, RT * sizeof(T), cudaMemcpyHostToDevice, s));
+    have_factors = true;
+  }
+  void get_factors(void* p) override {
+    CPF_CUDA_CHECK(cudaMemcpyAsync(p, A, RT * sizeof(T), cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+
+  void fit_begin(int variant, double tau, double tol, int max_iters, cpf_status* o) override {
+    require_ready();
+    if (variant < 0 || variant > 2) throw ApiError(CPF_E_ARG, "unknown variant");
+    reset_state(variant, 0.0, tol, max_iters);
+    if (trace_cap < max_iters) {
+      if (dtrace) CPF_CUDA_CHECK(cudaFree(dtrace));
+      dtrace = dalloc<IterRecordDev>(std::max(max_iters, 1));
+      trace_cap = max_iters;
+    }
+    // model = normalize_equal_energy(init)  (solver.py:321)
+    normalize(A, A, kAlways, 0);
+    pull_state();
+    if (hst->err_code == kErrZeroColumn) throw ApiError(CPF_E_ZERODIV, "component has a zero-norm vector");
+    // ||Y||; zero tensor -> ZeroDivisionError (solver.py:322-324)
+    const double ysq = ynorm_sq();
+    const double ynorm = std::sqrt(ysq);
+    if (ynorm == 0.0) throw ApiError(CPF_E_ZERODIV, "cannot fit a zero tensor");
+    // mu0 = tau * max(1, max Re diag C^(N)) of normalize_unit_modes(model) (solver.py:326-327, 229-235)
+    std::vector<double> hn((size_t)N * R);
+    launch(k_colnorms<T>, dim3(R, N), 256, 0, (const T*)A, md, norms, (const LmDeviceState*)st, (const DevFlags*)fl,
+           (int)kAlways);
+    CPF_CUDA_CHECK(cudaMemcpyAsync(hn.data(), norms, sizeof(double) * N * R, cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    double dmax = -INFINITY;
+    for (int r = 0; r < R; ++r) {
+      double sc = 1.0;
+      for (int n = 0; n < N - 1; ++n) sc = sc * hn[(size_t)n * R + r];
+      const double v = hn[(size_t)(N - 1) * R + r] * sc;
+      dmax = std::max(dmax, v * v);
+    }
+    const double mu0 = tau * std::max(1.0, dmax);
+    // cache, MTTKRPs, err (solver.py:329-332); error via ||Y||^2 - 2 Re<Y,X> + ||X||^2
+    build_cache_and_mttkrps(kAlways);
+    launch(k_xnorm2<T>, 1, 256, 0, (const T*)Cg, N, R, dscal + 2, (const LmDeviceState*)st, (const DevFlags*)fl,
+           (int)kAlways);
+    const double yx = host_yx_from(M, A);
+    double xx;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(&xx, dscal + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    const double res = std::max(ysq - 2.0 * yx + xx, 0.0);
+    const double err = std::sqrt(res) / ynorm;
+    hst->mu = mu0;
+    hst->growth = 2.0;
+    hst->err = err;
+    hst->err_sq = (err * ynorm) * (err * ynorm);
+    hst->ynorm = ynorm;
+    hst->ynorm_sq = ysq;
+    hst->variant = variant;
+    hst->tol = tol;
+    hst->max_iters = max_iters;
+    hst->stopped = max_iters <= 0 ? kStopMaxIters : 0;
+    // keep use_kinv computed by the cache kernels
+    LmDeviceState tmp;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(&tmp, st, sizeof(tmp), cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    hst->use_kinv = tmp.use_kinv;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(st, hst, sizeof(LmDeviceState), cudaMemcpyHostToDevice, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    fill_status(o);
+  }
+
+  static constexpr int kStopMaxIters = 4;
+
+  void iteration() {
+    const int g = kRunning;
+    candidate(2, g);
+    // delta' = cand - model (solver.py:348)
+    axpby(Cand, 1.0, A, -1.0, V1, g);
+    // normalised candidate: trial fit and, if accepted, the new model (solver.py:362)
+    normalize(Cand, Ac, g, 1);
+    cross_gram(Ac, Ac, Ccg, g);
+    launch(k_xnorm2<T>, 1, 256, 0, (const T*)Ccg, N, R, dscal + 2, (const LmDeviceState*)st, (const DevFlags*)fl, g);
+    pass_a(Ac, Mc, g);
+    launch(k_redot<T>, 1, 1024, 0, (const T*)(Ac + offs[0]), (const T*)(Mc + offs[0]), I1 * R, 0, dscal + 0,
+           (const LmDeviceState*)st, (const DevFlags*)fl, g);
+    launch(k_redot<T>, 1, 1024, 0, (const T*)V1, (const T*)G, RT, 1, dscal + 3, (const LmDeviceState*)st,
+           (const DevFlags*)fl, g);
+    launch(k_decide, 1, 1, 0, st, fl, dtrace, (const double*)dscal);
+    // commit an accepted candidate (solver.py:361-367): model, cache, MTTKRPs, gradient
+    const int ga = kOnAccept;
+    launch(k_copy<T>, nblocks(RT, 256), 256, 0, (const T*)Ac, A, RT, (const LmDeviceState*)st, (const DevFlags*)fl, ga);
+    launch(k_copy<T>, nblocks((int64_t)N * R * R, 256), 256, 0, (const T*)Ccg, Cg, (int64_t)N * R * R,
+           (const LmDeviceState*)st, (const DevFlags*)fl, ga);
+    cache_from_grams(Cg, ga);
+    launch(k_copy<T>, nblocks(offs[N - 1], 256), 256, 0, (const T*)Mc, M, offs[N - 1], (const LmDeviceState*)st,
+           (const DevFlags*)fl, ga);
+    pass_b(A, M, ga);
+    gradient(ga);
+    launch(k_clear_pending, 1, 1, 0, fl);
+  }
+
+  void fit_step(int n, cpf_status* o) override {
+    pull_state();
+    for (int k = 0; k < n && hst->stopped == 0; ++k) {
+      iteration();
+      pull_state();
+    }
+    fill_status(o);
+  }
+  int trace(cpf_iter_record* out, int cap) override {
+    pull_state();
+    const int cnt = std::min(cap, hst->iter);
+    std::vector<IterRecordDev> h(std::max(cnt, 1));
+    if (cnt > 0) {
+      CPF_CUDA_CHECK(cudaMemcpyAsync(h.data(), dtrace, sizeof(IterRecordDev) * cnt, cudaMemcpyDeviceToHost, s));
+      CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    for (int i = 0; i < cnt; ++i) {
+      out[i].iter = h[i].iter;
+      out[i].accepted = h[i].accepted;
+      out[i].relerr = h[i].relerr;
+      out[i].mu = h[i].mu;
+    }
+    return cnt;
+  }
+  void mttkrp(int mode, void* out) override {
+    require_ready();
+    reset_state(0, 0.0, 0.0, 0);
+    pass_a(A, M, kAlways);
+    pass_b(A, M, kAlways);
+    if (mode == 0) {
+      CPF_CUDA_CHECK(cudaMemcpyAsync(out, M, RT * sizeof(T), cudaMemcpyDeviceToHost, s));
+    } else {
+      if (mode < 1 || mode > N) throw ApiError(CPF_E_ARG, "mode out of range");
+      CPF_CUDA_CHECK(cudaMemcpyAsync(out, M + offs[mode - 1], dims[mode - 1] * R * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  double relative_error() override {
+    require_ready();
+    reset_state(0, 0.0, 0.0, 0);
+    const double ysq = ynorm_sq();
+    if (ysq == 0.0) throw ApiError(CPF_E_ZERODIV, "relative error undefined for a zero tensor");
+    cross_gram(A, A, Cg, kAlways);
+    launch(k_xnorm2<T>, 1, 256, 0, (const T*)Cg, N, R, dscal + 2, (const LmDeviceState*)st, (const DevFlags*)fl,
+           (int)kAlways);
+    pass_a(A, M, kAlways);
+    const double yx = host_yx_from(M, A);
+    double xx;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(&xx, dscal + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    return std::sqrt(std::max(ysq - 2.0 * yx + xx, 0.0)) / std::sqrt(ysq);
+  }
+  int flm_step(double mu, int variant, int refine, void* out) override {
+    require_ready();
+    reset_state(variant, mu, 0.0, 1);
+    build_cache_and_mttkrps(kAlways);
+    candidate(refine, kAlways);
+    pull_state();
+    if (hst->err_code) return hst->err_code;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(out, Cand, RT * sizeof(T), cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    return 0;
+  }
+  void profile(int on) override {
+    prof = on != 0;
+  }
+  void phase_times(double* ms, int64_t* cnt, int n) override {
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    for (auto& e : evs) {
+      float t = 0.f;
+      CPF_CUDA_CHECK(cudaEventElapsedTime(&t, e.a, e.b));
+      ph_ms[e.ph] += t;
+      ph_cnt[e.ph] += 1;
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    evs.clear();
+    for (int i = 0; i < n && i < kNumPhases; ++i) {
+      ms[i] = ph_ms[i];
+      cnt[i] = ph_cnt[i];
+    }
+  }
+  int64_t launches() const override { return nlaunch; }
+};
+
+}  // namespace cpf
+
+// ============================================================================================
+// C ABI (include/cpfast_b200.h)
+// ============================================================================================
+struct cpf_engine {
+  std::unique_ptr<cpf::EngineBase> impl;
+  std::string err;
+};
+
+namespace {
+thread_local std::string g_create_error;
+
+template <class F>
+int guarded(cpf_engine* e, F&& f) {
+  try {
+    f();
+    return CPF_OK;
+  } catch (const ApiError& x) {
+    if (e) e->err = x.what();
+    else g_create_error = x.what();
+    return x.code;
+  } catch (const CudaError& x) {
+    if (e) e->err = x.what();
+    else g_create_error = x.what();
+    return CPF_E_CUDA;
+  } catch (const std::exception& x) {
+    if (e) e->err = x.what();
+    else g_create_error = x.what();
+    return CPF_E_CUDA;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int cpf_abi_version(void) { return CPF_ABI_VERSION; }
+
+int cpf_device_count(int* n) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  if (n) *n = c;
+  return CPF_OK;
+}
+
+int cpf_nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return CPF_E_NCCL;
+  std::memcpy(out128, &id, sizeof(id));
+  return CPF_OK;
+}
+
+int cpf_engine_create(cpf_engine** out, int device, int kind, int order, const int64_t* dims, int rank,
+                      int world_rank, int world_size, const void* nccl_uid128) {
+  if (!out) return CPF_E_ARG;
+  *out = nullptr;
+  auto* e = new cpf_engine();
+  int rc = guarded(nullptr, [&] {
+    if (kind == CPF_REAL)
+      e->impl.reset(new cpf::Engine<double>(device, order, dims, rank, world_rank, world_size, nccl_uid128));
+    else if (kind == CPF_COMPLEX)
+      e->impl.reset(new cpf::Engine<cplx>(device, order, dims, rank, world_rank, world_size, nccl_uid128));
+    else
+      throw ApiError(CPF_E_KIND, "unknown scalar kind");
+  });
+  if (rc != CPF_OK) {
+    e->err = g_create_error;
+    *out = e;  // caller reads the message then destroys
+    return rc;
+  }
+  *out = e;
+  return CPF_OK;
+}
+
+void cpf_engine_destroy(cpf_engine* e) { delete e; }
+
+const char* cpf_engine_last_error(const cpf_engine* e) {
+  return e ? e->err.c_str() : g_create_error.c_str();
+}
+
+int cpf_engine_slab(const cpf_engine* e, int64_t* lo, int64_t* hi) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  e->impl->slab(lo, hi);
+  return CPF_OK;
+}
+
+void* cpf_engine_stream(cpf_engine* e) { return (e && e->impl) ? e->impl->stream() : nullptr; }
+
+int cpf_engine_set_tensor(cpf_engine* e, const void* data, int64_t nelem, int where) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->set_tensor(data, nelem, where); });
+}
+
+int cpf_engine_set_factors(cpf_engine* e, const void* stacked) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->set_factors(stacked); });
+}
+
+int cpf_engine_get_factors(cpf_engine* e, void* stacked) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->get_factors(stacked); });
+}
+
+int cpf_engine_fit_begin(cpf_engine* e, int variant, double tau, double tol, int max_iters, cpf_status* st) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->fit_begin(variant, tau, tol, max_iters, st); });
+}
+
+int cpf_engine_fit_step(cpf_engine* e, int n_iters, cpf_status* st) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->fit_step(n_iters, st); });
+}
+
+int cpf_engine_trace(cpf_engine* e, cpf_iter_record* out, int cap, int* n) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { *n = e->impl->trace(out, cap); });
+}
+
+int cpf_engine_mttkrp(cpf_engine* e, int mode, void* out) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->mttkrp(mode, out); });
+}
+
+int cpf_engine_relative_error(cpf_engine* e, double* out) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { *out = e->impl->relative_error(); });
+}
+
+int cpf_engine_flm_step(cpf_engine* e, double mu, int variant, int refine_steps, void* cand, int* err_code) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { *err_code = e->impl->flm_step(mu, variant, refine_steps, cand); });
+}
+
+int cpf_engine_profile(cpf_engine* e, int enable) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->profile(enable); });
+}
+
+int cpf_engine_phase_times(cpf_engine* e, double* ms_out, int64_t* counts_out, int nphases) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->phase_times(ms_out, counts_out, nphases); });
+}
+
+int64_t cpf_engine_launch_count(const cpf_engine* e) { return (e && e->impl) ? e->impl->launches() : 0; }
+
+}  // extern "C"

@@ -1,0 +1,424 @@
+// Dense LU with partial pivoting (getrf) and the triangular solves (getrs) for the fLM core
+// system Phi (phi.cuh).  The reference forms B = inv(Phi) with LAPACK getrf+getri
+// (hessian.py:207) or solve(I + Psi K, I) (hessian.py:209); here Phi is factored once per
+// iteration and B w is applied three times by forward/back substitution.
+//
+// Blocked right-looking algorithm, panel width KB:
+//   1. k_panel_lu   -- one thread-block CLUSTER owns the whole m x KB panel in distributed shared
+//                      memory.  Pivot search per column is a block reduction + one cluster
+//                      barrier: each CTA publishes its best candidate row into every CTA's smem
+//                      slot (double-buffered by column parity), so the chosen pivot row is
+//                      already local everywhere.  Rows are pivoted logically (retired), then
+//                      written back once in LAPACK order; the panel's row interchange is emitted
+//                      as a short gather list (<= 2 KB touched positions).
+//   2. k_row_gather -- applies that interchange to the columns outside the panel and to perm.
+//   3. k_trsm_llnu  -- U12 = L11^{-1} A12.
+//   4. k_gemm_sub   -- A22 -= L21 U12 (fp64 / complex128 tiled GEMM).
+// Solves: x = P b (gather by perm), then k_trsv<lower, unit> and k_trsv<upper> -- single-kernel
+// blocked substitution with per-block ready flags (decoupled look-back; CTAs take logical block
+// ids from an atomic ticket so every awaited block is already running).
+#pragma once
+#include <cooperative_groups.h>
+#include "cpf_common.cuh"
+
+namespace cpf {
+namespace cg = cooperative_groups;
+
+constexpr int kLuMaxCluster = 16;
+constexpr int kLuMaxKB = 32;
+
+// round kb up so the int arrays keep 16-byte alignment of the reduction scratch
+__host__ __device__ constexpr int kbMaxPad(int kb) { return (kb + 3) & ~3; }
+
+struct LuWork {
+  int* perm;       // n: final position -> original row
+  int* ipiv;       // n: LAPACK-style swap sequence (0-based positions)
+  int* gather;     // 2 * (2*KB): (pos, src) pairs of the current panel
+  int* gcount;     // 1
+  int* info;       // 1: first zero pivot (1-based), 0 = none
+  int* ticket;     // 2 counters for the substitution kernels
+  int* ready;      // ceil(n/32) flags
+};
+
+__global__ void k_lu_init(int* perm, int n, int* info) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) perm[i] = i;
+  if (i == 0) *info = 0;
+}
+
+template <class T>
+__global__ void k_panel_lu(T* __restrict__ A, int n, int lda, int k0, int kb, int rpc, LuWork w,
+                           const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // layout: panel [rpc x kb] T | cand_data [2][CL][kb] T | cand_val [2][CL] double |
+  //         cand_row [2][CL] int | retired [rpc] int | pivrows [kb] int | scratch
+  T* pan = reinterpret_cast<T*>(smem_raw);
+  T* cand_data = pan + (size_t)rpc * kb;
+  double* cand_val = reinterpret_cast<double*>(cand_data + 2 * CL * kb);
+  int* cand_row = reinterpret_cast<int*>(cand_val + 2 * CL);
+  int* retired = cand_row + 2 * CL;
+  int* pivrows = retired + rpc;
+  double* red_val = reinterpret_cast<double*>(((uintptr_t)(pivrows + kbMaxPad(kb)) + 15) & ~(uintptr_t)15);
+  int* red_idx = reinterpret_cast<int*>(red_val + 32);
+  int* bcast = red_idx + 32;  // [0] = local best index
+
+  const int m = n - k0;
+  const int row0 = rank * rpc;                 // first panel-relative row of this CTA
+  const int rows_here = max(0, min(rpc, m - row0));
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = (nthr + 31) >> 5;
+
+  // load panel rows [k0+row0, k0+row0+rows_here) x cols [k0, k0+kb)
+  for (int e = tid; e < rpc * kb; e += nthr) {
+    int i = e % rpc, q = e / rpc;
+    pan[e] = (i < rows_here) ? A[(int64_t)(k0 + row0 + i) + (int64_t)lda * (k0 + q)] : zero_of<T>();
+  }
+  for (int i = tid; i < rpc; i += nthr) retired[i] = (i < rows_here) ? 0 : 1;
+  __syncthreads();
+
+  for (int jj = 0; jj < kb; ++jj) {
+    const int par = jj & 1;
+    // ---- local argmax over non-retired rows (ties -> smaller row)
+    double bv = -1.0;
+    int bi = -1;
+    for (int i = tid; i < rows_here; i += nthr) {
+      if (retired[i]) continue;
+      double v = pivmag(pan[i + rpc * jj]);
+      if (v > bv) { bv = v; bi = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_down_sync(0xffffffffu, bv, o);
+      int oi = __shfl_down_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi >= 0 && (bi < 0 || oi < bi))) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { red_val[wid] = bv; red_idx[wid] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double b = red_val[0];
+      int ib = red_idx[0];
+      for (int q = 1; q < nw; ++q) {
+        double v = red_val[q];
+        int iq = red_idx[q];
+        if (v > b || (v == b && iq >= 0 && (ib < 0 || iq < ib))) { b = v; ib = iq; }
+      }
+      bcast[0] = ib;
+      // publish value and row index to every CTA
+      for (int r = 0; r < CL; ++r) {
+        double* rv = cluster.map_shared_rank(cand_val, r);
+        int* rr = cluster.map_shared_rank(cand_row, r);
+        rv[par * CL + rank] = b;
+        rr[par * CL + rank] = (ib >= 0) ? (k0 + row0 + ib) : 0x7fffffff;
+      }
+    }
+    __syncthreads();
+    {
+      const int ib = bcast[0];
+      for (int e = tid; e < kb * CL; e += nthr) {
+        int q = e % kb, r = e / kb;
+        T v = (ib >= 0) ? pan[ib + rpc * q] : zero_of<T>();
+        T* rd = cluster.map_shared_rank(cand_data, r);
+        rd[((size_t)par * CL + rank) * kb + q] = v;
+      }
+    }
+    cluster.sync();
+    // ---- choose the winner (identical in every CTA)
+    int win = 0;
+    {
+      double b = cand_val[par * CL];
+      int rw = cand_row[par * CL];
+      for (int r = 1; r < CL; ++r) {
+        double v = cand_val[par * CL + r];
+        int rr = cand_row[par * CL + r];
+        if (v > b || (v == b && rr < rw)) { b = v; rw = rr; win = r; }
+      }
+    }
+    const int wrow = cand_row[par * CL + win];  // absolute row index of the pivot
+    const T* prow = cand_data + ((size_t)par * CL + win) * kb;
+    const T piv = prow[jj];
+    const bool zero_piv = (pivmag(piv) == 0.0);
+    if (tid == 0) pivrows[jj] = wrow;
+    if (zero_piv && rank == 0 && tid == 0) {
+      if (*w.info == 0) *w.info = k0 + jj + 1;
+    }
+    const int wl = wrow - k0 - row0;  // local index if mine
+    const bool mine = (wl >= 0 && wl < rows_here);
+    // ---- eliminate below the pivot in my rows
+    for (int i = tid; i < rows_here; i += nthr) {
+      if (retired[i] || (mine && i == wl)) continue;
+      if (zero_piv) continue;
+      T l = dvd(pan[i + rpc * jj], piv);
+      pan[i + rpc * jj] = l;
+      for (int q = jj + 1; q < kb; ++q) fms_acc(pan[i + rpc * q], l, prow[q]);
+    }
+    if (mine && tid == 0) retired[wl] = 1;
+    __syncthreads();
+  }
+
+  // ---- LAPACK-order interchange: simulate swaps (pos k0+jj <-> current pos of pivot row)
+  // small maps of touched positions (<= 2 kb): tpos[t] -> orig row tval[t]
+  __shared__ int tpos[2 * kLuMaxKB], tval[2 * kLuMaxKB];
+  __shared__ int tcount;
+  if (tid == 0) {
+    int cnt = 0;
+    for (int jj = 0; jj < kb; ++jj) {
+      const int t = k0 + jj;
+      const int prow_abs = pivrows[jj];
+      // current position of prow_abs
+      int s = prow_abs;
+      for (int e = 0; e < cnt; ++e)
+        if (tval[e] == prow_abs) { s = tpos[e]; break; }
+      // orig rows at t and s
+      int et = -1, es = -1;
+      for (int e = 0; e < cnt; ++e) {
+        if (tpos[e] == t) et = e;
+        if (tpos[e] == s) es = e;
+      }
+      if (et < 0) { tpos[cnt] = t; tval[cnt] = t; et = cnt++; }
+      if (es < 0) { tpos[cnt] = s; tval[cnt] = s; es = cnt++; }
+      int tmp = tval[et];
+      tval[et] = tval[es];
+      tval[es] = tmp;
+      if (rank == 0) w.ipiv[t] = s;
+    }
+    tcount = cnt;
+    if (rank == 0) {
+      int g = 0;
+      for (int e = 0; e < cnt; ++e) {
+        if (tpos[e] == tval[e]) continue;  // fixed point
+        w.gather[2 * g] = tpos[e];
+        w.gather[2 * g + 1] = tval[e];
+        ++g;
+      }
+      *w.gcount = g;
+    }
+  }
+  __syncthreads();
+  // ---- write back my rows at their final positions
+  for (int e = tid; e < rows_here * kb; e += nthr) {
+    int i = e % rows_here, q = e / rows_here;
+    int orow = k0 + row0 + i;
+    int pos = orow;
+    for (int t = 0; t < tcount; ++t)
+      if (tval[t] == orow) { pos = tpos[t]; break; }
+    A[(int64_t)pos + (int64_t)lda * (k0 + q)] = pan[i + rpc * q];
+  }
+  cluster.sync();  // keep DSMEM alive until every CTA is done with remote slots
+}
+
+
+template <class T>
+size_t panel_smem_bytes(int rpc, int kb, int CL) {
+  size_t b = sizeof(T) * ((size_t)rpc * kb + 2 * (size_t)CL * kb);
+  b += sizeof(double) * 2 * CL + sizeof(int) * 2 * CL + sizeof(int) * rpc + sizeof(int) * kbMaxPad(kb);
+  b = (b + 15) & ~(size_t)15;
+  b += sizeof(double) * 32 + sizeof(int) * 32 + sizeof(int) * 4;
+  return b;
+}
+
+// Apply the panel's row gather (pos <- src) to columns [0,k0) U [k0+kb, n) and to perm.
+// Block: CB columns x G entries; first read all sources, barrier, then write.
+template <class T>
+__global__ void k_row_gather(T* __restrict__ A, int n, int lda, int k0, int kb, LuWork w, const LmDeviceState* st,
+                             int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int G = *w.gcount;
+  if (G == 0) return;
+  T* buf = reinterpret_cast<T*>(smem_raw);
+  __shared__ int pbuf[2 * kLuMaxKB];
+  const int ncols_out = n - kb;  // columns outside the panel
+  const int cb = blockDim.x / (2 * kLuMaxKB);
+  const int col_first = blockIdx.x * cb;
+  const int e = threadIdx.x % (2 * kLuMaxKB);
+  const int cl = threadIdx.x / (2 * kLuMaxKB);
+  const int cidx = col_first + cl;
+  // the last block also fixes perm (virtual column index ncols_out)
+  const bool do_col = (cidx < ncols_out) && (e < G);
+  int col = -1;
+  if (cidx < ncols_out) col = (cidx < k0) ? cidx : cidx + kb;
+  T v = zero_of<T>();
+  if (do_col) v = A[(int64_t)w.gather[2 * e + 1] + (int64_t)lda * col];
+  const bool do_perm = (blockIdx.x == 0) && (cl == 0) && (e < G);
+  int pv = 0;
+  if (do_perm) pv = w.perm[w.gather[2 * e + 1]];
+  buf[threadIdx.x] = v;
+  if (do_perm) pbuf[e] = pv;
+  __syncthreads();
+  if (do_col) A[(int64_t)w.gather[2 * e] + (int64_t)lda * col] = buf[threadIdx.x];
+  if (do_perm) w.perm[w.gather[2 * e]] = pbuf[e];
+}
+
+// U12 = L11^{-1} A12 (L11 unit lower, kb x kb); one thread per column of A12.
+template <class T, int KB>
+__global__ void k_trsm_llnu(T* __restrict__ A, int n, int lda, int k0, int kb, const LmDeviceState* st,
+                            int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  __shared__ T L[KB * KB];
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    int i = e % kb, j = e / kb;
+    L[i + KB * j] = A[(int64_t)(k0 + i) + (int64_t)lda * (k0 + j)];
+  }
+  __syncthreads();
+  const int col = k0 + kb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= n) return;
+  T x[KB];
+  T* a = A + (int64_t)lda * col + k0;
+#pragma unroll
+  for (int i = 0; i < KB; ++i) x[i] = (i < kb) ? a[i] : zero_of<T>();
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+    if (j >= kb) break;
+#pragma unroll
+    for (int i = j + 1; i < KB; ++i)
+      if (i < kb) fms_acc(x[i], L[i + KB * j], x[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < KB; ++i)
+    if (i < kb) a[i] = x[i];
+}
+
+// C -= A * B   (column-major; C: m x nn at (r0, c0); A = L21: m x k at (r0, k0); B = U12: k x nn at (k0, c0))
+// 64 x 64 tile, 256 threads, 4 x 4 outputs per thread (strided by 16 for conflict-free smem).
+template <class T>
+__global__ void __launch_bounds__(256) k_gemm_sub(T* __restrict__ Mx, int lda, int r0, int c0, int k0, int m, int nn,
+                                                  int k, const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  constexpr int TM = 64, TN = 64, BK = 16;
+  __shared__ T As[BK][TM + 1];
+  __shared__ T Bs[BK][TN + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int bm = blockIdx.x * TM, bn = blockIdx.y * TN;
+  T acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = zero_of<T>();
+  for (int kk = 0; kk < k; kk += BK) {
+    // load A tile: TM x BK  (rows bm.., cols kk..)
+    for (int e = threadIdx.x; e < TM * BK; e += 256) {
+      int i = e % TM, q = e / TM;
+      int gi = bm + i, gq = kk + q;
+      As[q][i] = (gi < m && gq < k) ? Mx[(int64_t)(r0 + gi) + (int64_t)lda * (k0 + gq)] : zero_of<T>();
+    }
+    for (int e = threadIdx.x; e < TN * BK; e += 256) {
+      int q = e % BK, j = e / BK;
+      int gj = bn + j, gq = kk + q;
+      Bs[q][j] = (gj < nn && gq < k) ? Mx[(int64_t)(k0 + gq) + (int64_t)lda * (c0 + gj)] : zero_of<T>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < BK; ++q) {
+      T a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[q][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[q][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fma_acc(acc[i][j], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int gi = bm + ty + 16 * i, gj = bn + tx + 16 * j;
+      if (gi < m && gj < nn) {
+        T* c = Mx + (int64_t)(r0 + gi) + (int64_t)lda * (c0 + gj);
+        *c = sub(*c, acc[i][j]);
+      }
+    }
+}
+
+// LU info -> engine error code (flm-a singular maps to the "I + Psi K" message)
+__global__ void k_lu_info_to_err(const int* info, LmDeviceState* st) {
+  if (st->stopped || st->err_code) return;
+  if (*info != 0) st->err_code = st->use_kinv ? kErrSingular : kErrPhi1Singular;
+}
+
+// x[q] = b[perm[q]]
+template <class T>
+__global__ void k_perm_gather(const T* __restrict__ b, const int* __restrict__ perm, int n, T* __restrict__ x,
+                              const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) x[q] = b[perm[q]];
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// In-place triangular solve on x (length n) with the LU factors in A.
+// LOWER: unit lower, forward.  !LOWER: upper (non-unit), backward.
+// Block = 4 warps; 32 rows per logical block.  ready[] holds the epoch of the last completion.
+template <class T, bool LOWER>
+__global__ void __launch_bounds__(128) k_trsv(const T* __restrict__ A, int n, int lda, T* __restrict__ x,
+                                              int* __restrict__ ticket, int* __restrict__ ready, int epoch,
+                                              const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  __shared__ int s_b;
+  __shared__ T part[4][32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_b = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int nblk = (n + 31) / 32;
+  const int lb = s_b;
+  const int blk = LOWER ? lb : (nblk - 1 - lb);
+  const int r0 = blk * 32;
+  const int rows = min(32, n - r0);
+  const int row = r0 + lane;
+  T acc = zero_of<T>();
+  // contributions from already-solved blocks: logical ids < lb, handled round-robin by warps
+  for (int q = wid; q < lb; q += 4) {
+    const int kblk = LOWER ? q : (nblk - 1 - q);
+    const int c0 = kblk * 32;
+    const int cols = min(32, n - c0);
+    if (lane == 0) {
+      while (ld_acquire_gpu(ready + kblk) != epoch) {
+      }
+    }
+    __syncwarp();
+    T xv = (lane < cols) ? ld_cg(x + c0 + lane) : zero_of<T>();
+    const bool rv = row < n;
+    for (int c = 0; c < cols; ++c) {
+      T xc = shfl_idx(xv, c);
+      if (rv) fms_acc(acc, A[(int64_t)row + (int64_t)lda * (c0 + c)], xc);
+    }
+  }
+  part[wid][lane] = acc;
+  __syncthreads();
+  if (wid == 0) {
+    T v = (row < n) ? ld_cg(x + row) : zero_of<T>();
+    v = add(v, add(add(part[0][lane], part[1][lane]), add(part[2][lane], part[3][lane])));
+    if (LOWER) {
+      for (int j = 0; j < rows; ++j) {
+        T yj = shfl_idx(v, j);
+        if (lane > j && lane < rows) fms_acc(v, A[(int64_t)row + (int64_t)lda * (r0 + j)], yj);
+      }
+    } else {
+      for (int j = rows - 1; j >= 0; --j) {
+        if (lane == j) v = dvd(v, A[(int64_t)row + (int64_t)lda * row]);
+        T yj = shfl_idx(v, j);
+        if (lane < j) fms_acc(v, A[(int64_t)row + (int64_t)lda * (r0 + j)], yj);
+      }
+    }
+    if (lane < rows) x[row] = v;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release_gpu(ready + blk, epoch);
+  }
+}
+
+}  // namespace cpf

@@ -1,0 +1,250 @@
+"""Drop-in fast damped Gauss-Newton (fLM) CP solver entry points, executed by the B200 engine.
+
+Mirrors ``cpfast.solver`` (cpfast/solver.py) and ``cpfast.complexcp`` (cpfast/complexcp.py):
+``FitConfig`` / ``IterRecord`` / ``FitResult`` have the same fields, defaults and validation;
+``fit`` / ``fit_complex`` / ``flm_step`` / ``mttkrp`` / ``relative_error`` have the same arguments,
+return types and error behaviour.  Every numerical step runs in hand-written sm_100a kernels
+behind the C ABI (include/cpfast_b200.h); the host only draws the seeded initial factors
+(bit-identical to the reference's ``default_rng([seed, 0])`` stream, kruskal.py:217-224) and
+assembles the result.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .tensor import COMPLEX, DenseTensor, KruskalModel, as_dense, as_model, model_from_vector, require_same_kind
+
+VARIANTS = ("flm-a", "flm-b", "auto", "als", "als-ls", "dgn-oracle")   # solver.py:44
+LM_VARIANTS = ("flm-a", "flm-b", "auto")
+MU_OVERFLOW = 1e30                                                       # solver.py:47
+RHO_DENOM_GUARD = 1e-30                                                  # solver.py:48
+POLL_EVERY = 1
+
+
+@dataclass
+class FitConfig:
+    """Same fields, defaults and validation as cpfast.solver.FitConfig (solver.py:62-76)."""
+
+    rank: int
+    variant: str = "auto"
+    tau: float = 1e-3
+    tol: float = 1e-8
+    max_iters: int = 1000
+    seed: int = 0
+    init: str = "svd"
+
+    def __post_init__(self):
+        if self.variant not in VARIANTS:
+            raise ValueError(f"unknown variant {self.variant!r}")
+        if self.rank < 1:
+            raise ValueError("rank must be >= 1")
+
+
+@dataclass
+class IterRecord:
+    iter: int
+    relerr: float
+    mu: float
+    accepted: bool
+
+
+@dataclass
+class FitResult:
+    model: KruskalModel
+    trace: list
+    stop_reason: str
+    time_ms: float = 0.0
+    launches: int = field(default=0, repr=False)
+
+    @property
+    def iters(self) -> int:
+        return len(self.trace)
+
+    @property
+    def accepted_iters(self) -> int:
+        return sum(1 for rec in self.trace if rec.accepted)
+
+    @property
+    def final_relerr(self) -> float:
+        return self.trace[-1].relerr if self.trace else float("nan")
+
+
+def _kind_code(arr) -> int:
+    return _native.CPF_COMPLEX if np.iscomplexobj(arr) else _native.CPF_REAL
+
+
+def random_init(dims, rank: int, rng, scalar_kind: str = "real") -> KruskalModel:
+    """N(0,1) factors drawn exactly like kruskal.py:217-224 (host RNG, bit-identical)."""
+    factors = []
+    for d in dims:
+        a = rng.standard_normal((d, rank))
+        if scalar_kind == COMPLEX:
+            a = a + 1j * rng.standard_normal((d, rank))
+        factors.append(a)
+    return KruskalModel(factors)
+
+
+def _init_model(y: DenseTensor, config: FitConfig, rng) -> KruskalModel:
+    if config.init == "random":
+        return random_init(y.dims, config.rank, rng, y.scalar_kind)
+    if config.init == "svd":
+        raise ValueError("init='svd' is not supported on the B200 backend yet; use init='random'")
+    raise ValueError(f"unknown init {config.init!r}")
+
+
+def _stop_reason(st) -> str:
+    if st.stopped == _native.STOP_TOL:
+        return "tol"
+    if st.stopped == _native.STOP_MU_OVERFLOW:
+        return "mu_overflow"
+    if st.stopped == _native.STOP_ERROR:
+        return f"error at iteration {st.err_iter}: {_native.ERR_MESSAGE.get(st.err_code, 'numerical error')}"
+    return "max_iters"
+
+
+class _Dist:
+    """Slab-sharding context for multi-GPU fits (one process per GPU, torch.distributed group)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def unique_id(self) -> bytes:
+        obj = [_native.nccl_unique_id() if self.rank == 0 else None]
+        self.dist.broadcast_object_list(obj, src=0, group=self.group)
+        return obj[0]
+
+
+def slab_bounds(dim_n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous slab of the last mode owned by ``rank`` (ceil split, same rule as the engine)."""
+    per = -(-dim_n // world)
+    lo = min(dim_n, per * rank)
+    return lo, min(dim_n, lo + per)
+
+
+def _make_engine(y: DenseTensor, rank: int, device, distributed):
+    dims = y.dims
+    if len(dims) < 2:
+        raise ValueError("the fLM solver needs a tensor of order >= 2")
+    dev = 0 if device is None else int(device)
+    if distributed is not None:
+        ctx = distributed if isinstance(distributed, _Dist) else _Dist(distributed if distributed is not True else None)
+        uid = ctx.unique_id() if ctx.world > 1 else None
+        eng = _native.Engine(_kind_code(y.data), dims, rank, dev, ctx.rank, ctx.world, uid)
+    else:
+        eng = _native.Engine(_kind_code(y.data), dims, rank, dev)
+    lo, hi = eng.slab
+    eng.set_tensor_host(y.data[..., lo:hi])
+    return eng
+
+
+def fit(y, config: FitConfig, *, device=None, distributed=None) -> FitResult:
+    """Decompose ``y`` with the fLM damped Gauss-Newton loop (solver.py:278-291, 319-384).
+
+    ``distributed``: None (single GPU), True (default torch.distributed group) or a process group;
+    the tensor is then slab-sharded along its last mode across the group's ranks, every rank
+    returns the same result.
+    """
+    t0 = time.monotonic()
+    if config.variant not in LM_VARIANTS:
+        raise ValueError(f"variant {config.variant!r} is not supported on the B200 backend "
+                         "(only the fast damped Gauss-Newton variants 'auto', 'flm-a', 'flm-b')")
+    y = as_dense(y)
+    rng = np.random.default_rng([config.seed, 0])
+    init = _init_model(y, config, rng)
+    eng = _make_engine(y, config.rank, device, distributed)
+    try:
+        eng.set_factors(init.as_vector())
+        st = eng.fit_begin(config.variant, config.tau, config.tol, config.max_iters)
+        while st.stopped == _native.STOP_RUNNING:
+            st = eng.fit_step(max(1, min(POLL_EVERY, config.max_iters)))
+        recs = eng.trace(config.max_iters)
+        trace = [IterRecord(t, e, m, a) for (t, e, m, a) in recs]
+        model = model_from_vector(eng.get_factors(), y.dims, config.rank)
+        result = FitResult(model, trace, _stop_reason(st), launches=eng.launch_count())
+        if st.stopped == _native.STOP_ERROR and st.err_code == _native.ERR_ZERO_COLUMN:
+            raise ZeroDivisionError("a component of the accepted candidate has a zero-norm vector")
+    finally:
+        eng.close()
+    result.time_ms = (time.monotonic() - t0) * 1e3
+    return result
+
+
+def fit_complex(y, config: FitConfig, **kw) -> FitResult:
+    """Complex fit: identical damping, stopping and normalisation (complexcp.py:51-54)."""
+    y = as_dense(y)
+    if y.scalar_kind != COMPLEX:
+        raise TypeError("expected a complex tensor")
+    return fit(y, config, **kw)
+
+
+def _model_engine(y: DenseTensor, model: KruskalModel, device):
+    if y.dims != model.dims:
+        raise ValueError(f"tensor dims {y.dims} do not match model {model.dims}")
+    require_same_kind(y.data, *model.factors)
+    eng = _make_engine(y, model.rank, device, None)
+    dtype = np.complex128 if np.iscomplexobj(y.data) else np.float64
+    eng.set_factors(np.concatenate([np.asarray(f, dtype=dtype).reshape(-1, order="F") for f in model.factors]))
+    return eng
+
+
+def mttkrp(y, model, n: int, *, device=None) -> np.ndarray:
+    """M_n = Y_(n) conj(KR_{k != n}) (kruskal.py:126-135), n is 1-based."""
+    y, model = as_dense(y), as_model(model)
+    if not 1 <= n <= model.order:
+        raise ValueError(f"mode {n} out of range for order-{model.order} tensor")
+    eng = _model_engine(y, model, device)
+    try:
+        out = eng.mttkrp(n)
+    finally:
+        eng.close()
+    return out.reshape((model.dims[n - 1], model.rank), order="F")
+
+
+def relative_error(y, model, *, device=None) -> float:
+    """||Y - X|| / ||Y|| (kruskal.py:159-167), weights folded into mode 1."""
+    y, model = as_dense(y), as_model(model)
+    if model.weights is not None:
+        f0 = model.factors[0] * model.weights[None, :]
+        model = KruskalModel([f0] + list(model.factors[1:]))
+    eng = _model_engine(y, model, device)
+    try:
+        return eng.relative_error()
+    finally:
+        eng.close()
+
+
+def flm_step(y, model, mu: float, variant: str = "auto", cache=None, mttkrps=None, refine_steps: int = 2,
+             *, device=None) -> KruskalModel:
+    """One fLM candidate with structured refinement (solver.py:189-226).
+
+    ``cache``/``mttkrps`` are accepted for signature compatibility; the engine recomputes them on
+    the device from ``model`` (they are pure functions of it).  Numerical failures raise like the
+    reference (numpy LinAlgError / SingularKernelError).
+    """
+    y, model = as_dense(y), as_model(model)
+    if variant not in LM_VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}")
+    eng = _model_engine(y, model, device)
+    try:
+        vec, code = eng.flm_step(mu, variant, refine_steps)
+    finally:
+        eng.close()
+    if code:
+        if code in (_native.ERR_KERNEL_SINGULAR, _native.ERR_PHI1_SINGULAR):
+            raise SingularKernelError(_native.ERR_MESSAGE[code])
+        raise np.linalg.LinAlgError(_native.ERR_MESSAGE.get(code, "numerical error"))
+    return model_from_vector(vec, model.dims, model.rank)
+
+
+class SingularKernelError(np.linalg.LinAlgError):
+    """The kernel matrix K is (numerically) singular (hessian.py:34-35)."""

@@ -1,0 +1,153 @@
+"""GPU parity: the sm_100a engine (through the drop-in API / C ABI) against the reference's golden
+fixtures and the CPU oracle.  Tolerances are the north-star's: identical accept/reject sequence and
+iteration count, factors within 1e-9 relative (Frobenius), final fit within 1e-10 absolute."""
+
+import numpy as np
+import pytest
+
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+FACTOR_RTOL = 1e-9
+FIT_ATOL = 1e-10
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def api(engine_lib):
+    import paper_1205_2584_b200 as api
+
+    return api
+
+
+def _model(api, case):
+    dims = tuple(int(x) for x in case["dims"])
+    r = int(case["rank"])
+    return api.KruskalModel(G.split_stacked(case["factors"], dims, r)), dims, r
+
+
+@pytest.mark.parametrize("cname", sorted(G.unit_cases()))
+def test_mttkrp_all_modes(api, cname):
+    case = G.unit_cases()[cname]
+    model, dims, r = _model(api, case)
+    y = api.DenseTensor(case["y"])
+    got = np.concatenate([api.mttkrp(y, model, n).reshape(-1, order="F") for n in range(1, len(dims) + 1)])
+    assert _rel(got, case["mttkrp"]) < 1e-13
+
+
+@pytest.mark.parametrize("cname", sorted(G.unit_cases()))
+def test_relative_error(api, cname):
+    case = G.unit_cases()[cname]
+    model, _, _ = _model(api, case)
+    got = api.relative_error(api.DenseTensor(case["y"]), model)
+    assert abs(got - float(case["relerr"])) < 1e-12
+
+
+@pytest.mark.parametrize("cname", sorted(G.unit_cases()))
+@pytest.mark.parametrize("variant", ["auto", "flm-a", "flm-b"])
+@pytest.mark.parametrize("mu", [1e-4, 0.1, 10.0])
+@pytest.mark.parametrize("refine", [0, 2])
+def test_flm_step(api, cname, variant, mu, refine):
+    case = G.unit_cases()[cname]
+    model, dims, r = _model(api, case)
+    key = f"step_{variant}_{mu:g}_{refine}"
+    y = api.DenseTensor(case["y"])
+    if key + "_error" in case:
+        with pytest.raises(np.linalg.LinAlgError):
+            api.flm_step(y, model, mu, variant, refine_steps=refine)
+        return
+    cand = api.flm_step(y, model, mu, variant, refine_steps=refine)
+    base = model.as_vector()
+    d_ref = case[key] - base
+    d_got = cand.as_vector() - base
+    assert _rel(d_got, d_ref) < 1e-8
+
+
+def _fit_golden(api, d, device=0):
+    from paper_1205_2584_b200 import synth
+
+    cfg = G.synth_config(d)
+    y = synth.make_tensor(cfg, d["seed"])
+    assert synth.tensor_digest(y) == d["digest"], "regenerated input differs from the golden input"
+    conf = api.FitConfig(rank=d["rank"], variant=d["variant"], tau=d["tau"], tol=d["tol"],
+                         max_iters=d["max_iters"], seed=d["seed"], init="random")
+    fitter = api.fit_complex if d["complex_"] else api.fit
+    return fitter(y, conf, device=device)
+
+
+def _tie_iters(d):
+    """Iterations whose reference decision margin is within 64 eps of err_sq."""
+    m = d["margins"]
+    if m.size == 0:
+        return set()
+    eps = np.finfo(float).eps
+    return {i + 1 for i, (esq, csq, _rho) in enumerate(m) if abs(esq - csq) <= 64 * eps * esq}
+
+
+@pytest.mark.parametrize("name", G.fit_names(include_full=False))
+def test_fit_matches_reference(api, name):
+    d = G.load_fit(name)
+    res = _fit_golden(api, d)
+    ref_seq = G.accept_seq(d["trace"])
+    got_seq = "".join("A" if r.accepted else "r" for r in res.trace)
+    ties = _tie_iters(d)
+    assert res.iters == len(d["trace"]), f"{got_seq} vs {ref_seq}"
+    assert res.stop_reason == d["stop_reason"]
+    mism = [i + 1 for i, (a, b) in enumerate(zip(got_seq, ref_seq)) if a != b]
+    assert all(t in ties for t in mism), f"non-tie decision mismatch at {mism}: {got_seq} vs {ref_seq}"
+    if not mism:
+        assert abs(res.final_relerr - d["trace"][-1, 1]) < FIT_ATOL
+        assert _rel(res.model.as_vector(), d["factors"]) < FACTOR_RTOL
+    # every recorded error matches through the last non-tie point
+    errs = np.array([r.relerr for r in res.trace])
+    first = min(mism) if mism else len(errs)
+    assert np.max(np.abs(errs[:first] - d["trace"][:first, 1])) < FIT_ATOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", [n for n in G.fit_names() if n not in G.fit_names(include_full=False)])
+def test_fit_matches_reference_full_config(api, name):
+    test_fit_matches_reference(api, name)
+
+
+@pytest.mark.parametrize("key", sorted(G.ensemble()))
+def test_ensemble_fit(api, key):
+    e = G.ensemble()[key]
+    variant = key.split("_", 1)[1]
+    y = api.DenseTensor(e["y"])
+    conf = api.FitConfig(rank=int(e["rank"]), variant=variant, tol=1e-10, max_iters=40, seed=int(e["seed"]),
+                         init="random")
+    res = api.fit(y, conf)
+    ref = e["trace"]
+    assert res.stop_reason == str(e["stop"])
+    assert res.iters == len(ref)
+    accepted = [r.relerr for r in res.trace if r.accepted]
+    assert all(b < a for a, b in zip(accepted, accepted[1:]))
+    # tiny ensemble problems converge to exact-fit level; compare the fit trajectory
+    errs = np.array([r.relerr for r in res.trace])
+    assert np.max(np.abs(errs - ref[:, 1])) < 1e-8
+
+
+def test_zero_tensor_raises(api):
+    with pytest.raises(ZeroDivisionError):
+        api.fit(api.DenseTensor(np.zeros((3, 3, 3))), api.FitConfig(rank=1, init="random"))
+
+
+def test_fit_complex_rejects_real(api):
+    with pytest.raises(TypeError):
+        api.fit_complex(api.DenseTensor(np.ones((3, 3))), api.FitConfig(rank=1, init="random"))
+
+
+def test_flm_b_singular_kernel_is_error_stop(api):
+    # orthonormal factors make every off-diagonal Gamma^(n,m) entry vanish -> K singular
+    rng = np.random.default_rng(5)
+    fac = [np.linalg.qr(rng.standard_normal((4, 2)))[0] for _ in range(3)]
+    x = np.einsum("ir,jr,kr->ijk", *fac)
+    y = api.DenseTensor(x + 1e-3 * rng.standard_normal(x.shape))
+    model = api.KruskalModel(fac)
+    with pytest.raises(api.SingularKernelError):
+        api.flm_step(y, model, 0.1, "flm-b")
