@@ -181,7 +181,8 @@ struct LmDeviceState {
   int variant;               // 0 auto, 1 flm-a, 2 flm-b
   int max_iters;
   int cand_zero;             // normalised candidate had a zero-norm column (raise on accept)
-  int pad_[3];
+  int err_direct;            // err/err_sq come from a direct residual (not the identity)
+  int pad_[2];
 };
 
 struct IterRecordDev {

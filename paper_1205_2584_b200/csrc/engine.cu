@@ -97,6 +97,7 @@ struct Engine final : EngineBase {
   T *W1 = nullptr, *Sm = nullptr;
   T *wvec = nullptr, *fvec = nullptr, *xvec = nullptr, *Phi = nullptr;
   T *A1c = nullptr, *KMc = nullptr, *WNc = nullptr, *zpart = nullptr, *m1part = nullptr, *bpart = nullptr;
+  T *A1r = nullptr, *KMr = nullptr, *WNr = nullptr;  // non-conj operands of the direct residual
   T *pa_out = nullptr, *pb_out = nullptr, *pb_all = nullptr;
   double *norms = nullptr, *dscal = nullptr, *red = nullptr;
   int* ibuf = nullptr;
@@ -179,7 +180,7 @@ struct Engine final : EngineBase {
     if (s) cudaStreamSynchronize(s);
     for (auto& e : evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     void* ptrs[] = {Yown, A, Ac, M, Mc, D, G, Cand, V1, V2, V3, V4, Cg, Ccg, Gx, Gp, Gf, Gti, Gi, W1, Sm,
-                    wvec, fvec, xvec, Phi, A1c, KMc, WNc, zpart, m1part, bpart, pa_out, pb_out, pb_all,
+                    wvec, fvec, xvec, Phi, A1c, KMc, WNc, A1r, KMr, WNr, zpart, m1part, bpart, pa_out, pb_out, pb_all,
                     norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok};
     for (void* p : ptrs)
       if (p) cudaFree(p);
@@ -208,6 +209,9 @@ struct Engine final : EngineBase {
     A1c = dalloc<T>((size_t)I1 * RP);
     KMc = dalloc<T>((size_t)Lmid * RP);
     WNc = dalloc<T>((size_t)std::max<int64_t>(Cloc, 1) * RP);
+    A1r = dalloc<T>((size_t)I1 * RP);
+    KMr = dalloc<T>((size_t)Lmid * RP);
+    WNr = dalloc<T>((size_t)std::max<int64_t>(Cloc, 1) * RP);
     pa_out = dalloc<T>((size_t)(I1 + Lmid) * R);
     pb_out = dalloc<T>((size_t)Cpad * R);
     pb_all = dalloc<T>((size_t)Cpad * R * world);
@@ -347,14 +351,14 @@ struct Engine final : EngineBase {
 
   // conj row-major operand copies for factors F (stacked)
   void prep_operands(const T* F, bool need_wn, int gate) {
-    launch(k_conj_rowmajor<T>, nblocks(I1 * RP, 256), 256, 0, F + offs[0], I1, (int64_t)0, I1, R, RP, A1c, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    launch(k_conj_rowmajor<T>, nblocks(I1 * RP, 256), 256, 0, F + offs[0], I1, (int64_t)0, I1, R, RP, A1c, (const LmDeviceState*)st, (const DevFlags*)fl, gate, 1);
     if (N == 3) {
-      launch(k_conj_rowmajor<T>, nblocks(Lmid * RP, 256), 256, 0, F + offs[1], Lmid, (int64_t)0, Lmid, R, RP, KMc, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+      launch(k_conj_rowmajor<T>, nblocks(Lmid * RP, 256), 256, 0, F + offs[1], Lmid, (int64_t)0, Lmid, R, RP, KMc, (const LmDeviceState*)st, (const DevFlags*)fl, gate, 1);
     } else {
-      launch(k_krmid<T>, nblocks(Lmid * RP, 256), 256, 0, (const T*)F, mg, Lmid, R, RP, KMc, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+      launch(k_krmid<T>, nblocks(Lmid * RP, 256), 256, 0, (const T*)F, mg, Lmid, R, RP, KMc, (const LmDeviceState*)st, (const DevFlags*)fl, gate, 1);
     }
     if (need_wn && Cloc > 0)
-      launch(k_conj_rowmajor<T>, nblocks(Cloc * RP, 256), 256, 0, F + offs[N - 1], Cloc, slab_lo, IN, R, RP, WNc, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+      launch(k_conj_rowmajor<T>, nblocks(Cloc * RP, 256), 256, 0, F + offs[N - 1], Cloc, slab_lo, IN, R, RP, WNc, (const LmDeviceState*)st, (const DevFlags*)fl, gate, 1);
   }
 
   // Pass A at factors F -> out modes 1..N-1 of Mout (stacked), allreduced.
@@ -420,6 +424,33 @@ struct Engine final : EngineBase {
                Mout + offs[N - 1] + lo, IN, cnt_rows, (int64_t)R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
       }
     }
+  }
+
+  // ||Y - X(F)||^2 computed directly (guard band, preamble, relative_error API) -> *out (device)
+  void direct_resid(const T* F, double* out, int gate) {
+    const LmDeviceState* cst = st;
+    const DevFlags* cfl = fl;
+    launch(k_conj_rowmajor<T>, nblocks(I1 * RP, 256), 256, 0, F + offs[0], I1, (int64_t)0, I1, R, RP, A1r, cst, cfl, gate, 0);
+    if (N == 3)
+      launch(k_conj_rowmajor<T>, nblocks(Lmid * RP, 256), 256, 0, F + offs[1], Lmid, (int64_t)0, Lmid, R, RP, KMr, cst,
+             cfl, gate, 0);
+    else
+      launch(k_krmid<T>, nblocks(Lmid * RP, 256), 256, 0, F, mg, Lmid, R, RP, KMr, cst, cfl, gate, 0);
+    if (Cloc > 0) {
+      launch(k_conj_rowmajor<T>, nblocks(Cloc * RP, 256), 256, 0, F + offs[N - 1], Cloc, slab_lo, IN, R, RP, WNr, cst,
+             cfl, gate, 0);
+      const int nb = (int)std::min<int64_t>(1024, std::max<int64_t>(1, nblocks(Lrows, 256)));
+      dispatch_rp([&](auto rpc) {
+        constexpr int RPc = decltype(rpc)::value;
+        launch(k_direct_resid<T, RPc>, nb, 256, sizeof(T) * kPassCK * RPc, Y, I1, Lmid, Cloc, (const T*)WNr,
+               (const T*)A1r, (const T*)KMr, red, cst, cfl, gate);
+      });
+      launch(k_sum_partials, 1, 1024, 0, (const double*)red, nb, out, cst, cfl, gate);
+    } else {
+      launch(k_axpby<double>, 1, 1, 0, (const double*)out, 0.0, (const double*)nullptr, 0.0, out, (int64_t)1, cst, cfl,
+             gate);
+    }
+    if (world > 1) NCCL_CHECK(ncclAllReduce(out, out, 1, ncclDouble, ncclSum, comm, s));
   }
 
   // ------------------------------------------------------------------------------------------
@@ -590,7 +621,7 @@ struct Engine final : EngineBase {
     const int nb = 1024;
     if (Jloc > 0) {
       launch(k_sumsq_partial<T>, nb, 256, 0, Y, Jloc, red);
-      launch(k_sum_partials, 1, 1024, 0, (const double*)red, nb, dscal + 1);
+      launch(k_sum_partials, 1, 1024, 0, (const double*)red, nb, dscal + 1, (const LmDeviceState*)nullptr, (const DevFlags*)nullptr, 0);
     } else {
       CPF_CUDA_CHECK(cudaMemsetAsync(dscal + 1, 0, sizeof(double), s));
     }
@@ -700,12 +731,12 @@ struct Engine final : EngineBase {
     build_cache_and_mttkrps(kAlways);
     launch(k_xnorm2<T>, 1, 256, 0, (const T*)Cg, N, R, dscal + 2, (const LmDeviceState*)st, (const DevFlags*)fl,
            (int)kAlways);
-    const double yx = host_yx_from(M, A);
-    double xx;
-    CPF_CUDA_CHECK(cudaMemcpyAsync(&xx, dscal + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    direct_resid(A, dscal + 5, kAlways);
+    double res;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(&res, dscal + 5, sizeof(double), cudaMemcpyDeviceToHost, s));
     CPF_CUDA_CHECK(cudaStreamSynchronize(s));
-    const double res = std::max(ysq - 2.0 * yx + xx, 0.0);
     const double err = std::sqrt(res) / ynorm;
+    hst->err_direct = 1;
     hst->mu = mu0;
     hst->growth = 2.0;
     hst->err = err;
@@ -742,6 +773,9 @@ struct Engine final : EngineBase {
            (const LmDeviceState*)st, (const DevFlags*)fl, g);
     launch(k_redot<T>, 1, 1024, 0, (const T*)V1, (const T*)G, RT, 1, dscal + 3, (const LmDeviceState*)st,
            (const DevFlags*)fl, g);
+    launch(k_precheck, 1, 1, 0, (const LmDeviceState*)st, fl, (const double*)dscal);
+    direct_resid(Ac, dscal + 4, kOnDirect);
+    direct_resid(A, dscal + 5, kOnCurDirect);
     launch(k_decide, 1, 1, 0, st, fl, dtrace, (const double*)dscal);
     // commit an accepted candidate (solver.py:361-367): model, cache, MTTKRPs, gradient
     const int ga = kOnAccept;
@@ -798,15 +832,11 @@ struct Engine final : EngineBase {
     reset_state(0, 0.0, 0.0, 0);
     const double ysq = ynorm_sq();
     if (ysq == 0.0) throw ApiError(CPF_E_ZERODIV, "relative error undefined for a zero tensor");
-    cross_gram(A, A, Cg, kAlways);
-    launch(k_xnorm2<T>, 1, 256, 0, (const T*)Cg, N, R, dscal + 2, (const LmDeviceState*)st, (const DevFlags*)fl,
-           (int)kAlways);
-    pass_a(A, M, kAlways);
-    const double yx = host_yx_from(M, A);
-    double xx;
-    CPF_CUDA_CHECK(cudaMemcpyAsync(&xx, dscal + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    direct_resid(A, dscal + 5, kAlways);
+    double res;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(&res, dscal + 5, sizeof(double), cudaMemcpyDeviceToHost, s));
     CPF_CUDA_CHECK(cudaStreamSynchronize(s));
-    return std::sqrt(std::max(ysq - 2.0 * yx + xx, 0.0)) / std::sqrt(ysq);
+    return std::sqrt(res) / std::sqrt(ysq);
   }
   int flm_step(double mu, int variant, int refine, void* out) override {
     require_ready();

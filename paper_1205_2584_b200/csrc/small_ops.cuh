@@ -22,18 +22,23 @@ struct Modes {
 };
 
 // Kernel gating.  kAlways: unconditional (preamble); kRunning: skip once the fit stopped;
-// kOnAccept: only while an accepted candidate is being committed (state->pending_accept).
-enum Gate : int { kAlways = 0, kRunning = 1, kOnAccept = 2 };
+// kOnAccept: only while an accepted candidate is being committed (flags->pending_accept);
+// kOnDirect / kOnCurDirect: the guard-band direct residual of the candidate / current model.
+enum Gate : int { kAlways = 0, kRunning = 1, kOnAccept = 2, kOnDirect = 3, kOnCurDirect = 4 };
 
 struct DevFlags {
   int pending_accept;
-  int pad[3];
+  int need_direct;
+  int need_cur_direct;
+  int pad;
 };
 
 __device__ __forceinline__ bool gate_open(const LmDeviceState* st, const DevFlags* fl, int gate) {
   if (gate == kAlways) return true;
   if (gate == kRunning) return st->stopped == 0;
-  return fl->pending_accept != 0;
+  if (gate == kOnAccept) return fl->pending_accept != 0;
+  if (gate == kOnDirect) return fl->need_direct != 0;
+  return fl->need_cur_direct != 0;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -506,7 +511,9 @@ __global__ void k_sumsq_partial(const T* __restrict__ y, int64_t n, double* __re
   if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
-__global__ void k_sum_partials(const double* __restrict__ part, int n, double* __restrict__ outp) {
+__global__ void k_sum_partials(const double* __restrict__ part, int n, double* __restrict__ outp,
+                               const LmDeviceState* st = nullptr, const DevFlags* fl = nullptr, int gate = 0) {
+  if (gate && !gate_open(st, fl, gate)) return;
   __shared__ double scratch[32];
   double acc = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) acc += part[i];
@@ -536,6 +543,25 @@ __global__ void k_copy2d(const T* __restrict__ src, int64_t lds, T* __restrict__
 
 __global__ void k_clear_pending(DevFlags* fl) { fl->pending_accept = 0; }
 
+// Guard band: the identity ||Y||^2 - 2Re<Y,X> + ||X||^2 has an absolute error of a
+// few eps * ||Y||^2.  When the accept decision is within that band of a tie, or the residual is
+// so small that the identity cannot resolve it (exact-fit problems), the candidate's residual --
+// and, once, the current model's -- is recomputed directly from Y (k_direct_resid).
+__global__ void k_precheck(const LmDeviceState* st, DevFlags* fl, const double* scal) {
+  if (st->stopped || st->err_code) {
+    fl->need_direct = 0;
+    fl->need_cur_direct = 0;
+    return;
+  }
+  const double yx = scal[0], xx = scal[2];
+  const double cs = st->ynorm_sq - 2.0 * yx + xx;
+  const double scale_ = st->ynorm_sq + fabs(xx) + 2.0 * fabs(yx);
+  const bool tiny = cs < 1e-10 * st->ynorm_sq;
+  const bool close = fabs(st->err_sq - cs) <= 1e-12 * scale_;
+  fl->need_direct = (tiny || close) ? 1 : 0;
+  fl->need_cur_direct = (fl->need_direct && !st->err_direct) ? 1 : 0;
+}
+
 // One LM decision (solver.py:354-383): trial error from the identity
 //   ||Y - X||^2 = ||Y||^2 - 2 Re<Y,X> + ||X||^2,
 // gain ratio (solver.py:259-263), Nielsen update (solver.py:238-248), accept test, trace record,
@@ -550,7 +576,17 @@ __global__ void k_decide(LmDeviceState* st, DevFlags* fl, IterRecordDev* trace, 
     return;
   }
   const double yx = scal[0], xx = scal[2], denom = scal[3];
-  const double raw = st->ynorm_sq - 2.0 * yx + xx;
+  const bool direct = fl->need_direct != 0;
+  if (fl->need_cur_direct) {  // re-anchor the current error on a direct residual (kruskal.py:159-167)
+    const double e0 = sqrt(scal[5]) / st->ynorm;
+    const double es = e0 * st->ynorm;
+    st->err = e0;
+    st->err_sq = es * es;
+    st->err_direct = 1;
+  }
+  fl->need_direct = 0;
+  fl->need_cur_direct = 0;
+  const double raw = direct ? scal[4] : st->ynorm_sq - 2.0 * yx + xx;
   const double cand_err = sqrt(fmax(raw, 0.0)) / st->ynorm;
   const double cs = cand_err * st->ynorm;
   const double cand_sq = cs * cs;
@@ -590,6 +626,7 @@ __global__ void k_decide(LmDeviceState* st, DevFlags* fl, IterRecordDev* trace, 
     d = fabs(st->err - cand_err);
     st->err = cand_err;
     st->err_sq = cand_sq;
+    st->err_direct = direct ? 1 : 0;
     acc = 1;
     fl->pending_accept = 1;
   } else {

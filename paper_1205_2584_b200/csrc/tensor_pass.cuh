@@ -24,13 +24,15 @@ namespace cpf {
 // Row-major conj copies used by the passes: dst[i*RP + r] = conj(src[i + ld*r]) (r<R), 0 pad.
 template <class T>
 __global__ void k_conj_rowmajor(const T* __restrict__ src, int64_t rows, int64_t row0, int64_t ld, int R, int RP,
-                                T* __restrict__ dst, const LmDeviceState* st, const DevFlags* fl, int gate) {
+                                T* __restrict__ dst, const LmDeviceState* st, const DevFlags* fl, int gate,
+                                int do_conj = 1) {
   if (!gate_open(st, fl, gate)) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= rows * RP) return;
   int64_t i = idx / RP;
   int r = (int)(idx % RP);
-  dst[idx] = r < R ? cj(src[(row0 + i) + ld * r]) : zero_of<T>();
+  T v = r < R ? src[(row0 + i) + ld * r] : zero_of<T>();
+  dst[idx] = do_conj ? cj(v) : v;
 }
 
 // KRmid[m, r] = prod_{k=2..N-1} A_k[i_k(m), r]  (conj, row-major, padded).  m: mode 2 fastest.
@@ -42,7 +44,7 @@ struct MidGeom {
 
 template <class T>
 __global__ void k_krmid(const T* __restrict__ A, MidGeom g, int64_t Lmid, int R, int RP, T* __restrict__ dst,
-                        const LmDeviceState* st, const DevFlags* fl, int gate) {
+                        const LmDeviceState* st, const DevFlags* fl, int gate, int do_conj = 1) {
   if (!gate_open(st, fl, gate)) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= Lmid * RP) return;
@@ -56,7 +58,7 @@ __global__ void k_krmid(const T* __restrict__ A, MidGeom g, int64_t Lmid, int R,
     rem /= g.dims[k];
     v = k == 0 ? A[g.offs[k] + ik + g.dims[k] * r] : mul(v, A[g.offs[k] + ik + g.dims[k] * r]);
   }
-  dst[idx] = cj(v);
+  dst[idx] = do_conj ? cj(v) : v;
 }
 
 constexpr int kPassCK = 32;  // W rows staged in shared memory per step
@@ -313,6 +315,47 @@ __global__ void k_mid_mttkrp(const T* __restrict__ Z, int64_t Lmid, const T* __r
     fma_cacc(acc, kr, Z[m + Lmid * r]);
   }
   Mn[idx] = acc;
+}
+
+// Direct residual ||Y - X||^2 (guard band and relative_error API; kruskal.py:159-167).
+// Thread per row l = i1 + I1*m: p[r] = A_1[i1,r] KRmid[m,r] (non-conj), then for every local c
+// x = sum_r p[r] A_N[c,r] and acc += |y - x|^2.  Per-block partials, fixed order.
+template <class T, int RP>
+__global__ void __launch_bounds__(256) k_direct_resid(const T* __restrict__ Y, int64_t I1, int64_t Lmid, int64_t C,
+                                                      const T* __restrict__ WN, const T* __restrict__ A1r,
+                                                      const T* __restrict__ KM, double* __restrict__ part,
+                                                      const LmDeviceState* st, const DevFlags* fl, int gate) {
+  if (!gate_open(st, fl, gate)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* w_s = reinterpret_cast<T*>(smem_raw);
+  __shared__ double scratch[32];
+  const int64_t Lrows = I1 * Lmid;
+  double acc = 0.0;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < Lrows; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = base + threadIdx.x;
+    const bool ok = l < Lrows;
+    T p[RP];
+    if (ok) {
+      const int64_t i1 = l % I1, m = l / I1;
+#pragma unroll
+      for (int r = 0; r < RP; ++r) p[r] = mul(A1r[i1 * RP + r], KM[m * RP + r]);
+    }
+    for (int64_t c0 = 0; c0 < C; c0 += kPassCK) {
+      const int ck = (int)(C - c0 < (int64_t)kPassCK ? C - c0 : (int64_t)kPassCK);
+      __syncthreads();
+      for (int e = threadIdx.x; e < ck * RP; e += blockDim.x) w_s[e] = WN[c0 * RP + e];
+      __syncthreads();
+      if (ok)
+        for (int k = 0; k < ck; ++k) {
+          T x = zero_of<T>();
+#pragma unroll
+          for (int r = 0; r < RP; ++r) fma_acc(x, p[r], w_s[k * RP + r]);
+          acc += abs2(sub(Y[l + Lrows * (c0 + k)], x));
+        }
+    }
+  }
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
 }  // namespace cpf
