@@ -449,7 +449,7 @@ class OracleResult:
         return self.trace[-1][1] if self.trace else float("nan")
 
 
-def fit_lm(y, cfg: OracleConfig, init_factors=None) -> OracleResult:
+def fit_lm(y, cfg: OracleConfig, init_factors=None, on_iter=None) -> OracleResult:
     """The damped Gauss-Newton loop, semantics of solver.py:319-384 (Appendix A of SURVEY)."""
     t0 = time.monotonic()
     y = fortran_tensor(y)
@@ -474,6 +474,8 @@ def fit_lm(y, cfg: OracleConfig, init_factors=None) -> OracleResult:
     err_sq = (err * ynorm) ** 2
     trace, deltas, detail = [], [], []
     stop = "max_iters"
+    if on_iter is not None:
+        on_iter(0)
     for t in range(1, cfg.max_iters + 1):
         try:
             cand = flm_candidate(A, mu, cfg.variant, g, M)
@@ -498,6 +500,8 @@ def fit_lm(y, cfg: OracleConfig, init_factors=None) -> OracleResult:
             deltas.append(0.0)
             accepted = False
         trace.append((t, err, mu, accepted))
+        if on_iter is not None:
+            on_iter(t)
         if len(deltas) >= 10 and all(d < cfg.tol for d in deltas[-10:]):
             stop = "tol"
             break

@@ -371,12 +371,13 @@ struct Engine final : EngineBase {
         launch(k_pass_a<T, RPc>, dim3(pa_tiles, pa_groups), dim3(pa_threads), pa_smem, Y, I1, Lmid, Cloc,
                (const T*)WNc, (const T*)A1c, (const T*)KMc, pa_TI, pa_TM, pa_mper, zpart, m1part, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
       });
+      ph_end();
       launch(k_pass_a_reduce<T>, nblocks((I1 + Lmid) * R, 256), 256, 0, (const T*)m1part, pa_groups,
              (const T*)zpart, pa_tiles, I1, Lmid, R, RP, pa_out, pa_out + I1 * R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
     } else {
+      ph_end();
       CPF_CUDA_CHECK(cudaMemsetAsync(pa_out, 0, sizeof(T) * (I1 + Lmid) * R, s));
     }
-    ph_end();
     if (world > 1) {
       NCCL_CHECK(ncclAllReduce(pa_out, pa_out, (size_t)(I1 + Lmid) * R * (sizeof(T) / sizeof(double)), ncclDouble,
                                ncclSum, comm, s));

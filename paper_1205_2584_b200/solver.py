@@ -89,7 +89,14 @@ def random_init(dims, rank: int, rng, scalar_kind: str = "real") -> KruskalModel
     return KruskalModel(factors)
 
 
-def _init_model(y: DenseTensor, config: FitConfig, rng) -> KruskalModel:
+class _Dims:
+    """dims + scalar kind of the (possibly sharded) tensor, for the host-side init draw."""
+
+    def __init__(self, dims, kind):
+        self.dims, self.scalar_kind = tuple(dims), kind
+
+
+def _init_model(y, config: FitConfig, rng) -> KruskalModel:
     if config.init == "random":
         return random_init(y.dims, config.rank, rng, y.scalar_kind)
     if config.init == "svd":
@@ -131,8 +138,8 @@ def slab_bounds(dim_n: int, world: int, rank: int) -> tuple[int, int]:
     return lo, min(dim_n, lo + per)
 
 
-def _make_engine(y: DenseTensor, rank: int, device, distributed):
-    dims = y.dims
+def _make_engine(y: DenseTensor, rank: int, device, distributed, slab_of=None):
+    dims = y.dims if slab_of is None else tuple(y.dims[:-1]) + (int(slab_of),)
     if len(dims) < 2:
         raise ValueError("the fLM solver needs a tensor of order >= 2")
     dev = 0 if device is None else int(device)
@@ -143,25 +150,33 @@ def _make_engine(y: DenseTensor, rank: int, device, distributed):
     else:
         eng = _native.Engine(_kind_code(y.data), dims, rank, dev)
     lo, hi = eng.slab
-    eng.set_tensor_host(y.data[..., lo:hi])
+    if slab_of is None:
+        eng.set_tensor_host(y.data[..., lo:hi])
+    else:
+        if y.dims[-1] != hi - lo:
+            raise ValueError(f"local slab has {y.dims[-1]} slices, this rank owns [{lo}, {hi})")
+        eng.set_tensor_host(y.data)
     return eng
 
 
-def fit(y, config: FitConfig, *, device=None, distributed=None) -> FitResult:
+def fit(y, config: FitConfig, *, device=None, distributed=None, slab_of=None) -> FitResult:
     """Decompose ``y`` with the fLM damped Gauss-Newton loop (solver.py:278-291, 319-384).
 
     ``distributed``: None (single GPU), True (default torch.distributed group) or a process group;
     the tensor is then slab-sharded along its last mode across the group's ranks, every rank
-    returns the same result.
+    returns the same result.  ``slab_of``: when given (the global size of the last mode), ``y``
+    holds only this rank's slab of the last mode (``slab_bounds``), so no rank needs the whole
+    tensor in host memory.
     """
     t0 = time.monotonic()
     if config.variant not in LM_VARIANTS:
         raise ValueError(f"variant {config.variant!r} is not supported on the B200 backend "
                          "(only the fast damped Gauss-Newton variants 'auto', 'flm-a', 'flm-b')")
     y = as_dense(y)
+    gdims = y.dims if slab_of is None else tuple(y.dims[:-1]) + (int(slab_of),)
     rng = np.random.default_rng([config.seed, 0])
-    init = _init_model(y, config, rng)
-    eng = _make_engine(y, config.rank, device, distributed)
+    init = _init_model(_Dims(gdims, y.scalar_kind), config, rng)
+    eng = _make_engine(y, config.rank, device, distributed, slab_of)
     try:
         eng.set_factors(init.as_vector())
         st = eng.fit_begin(config.variant, config.tau, config.tol, config.max_iters)
@@ -169,7 +184,7 @@ def fit(y, config: FitConfig, *, device=None, distributed=None) -> FitResult:
             st = eng.fit_step(max(1, min(POLL_EVERY, config.max_iters)))
         recs = eng.trace(config.max_iters)
         trace = [IterRecord(t, e, m, a) for (t, e, m, a) in recs]
-        model = model_from_vector(eng.get_factors(), y.dims, config.rank)
+        model = model_from_vector(eng.get_factors(), gdims, config.rank)
         result = FitResult(model, trace, _stop_reason(st), launches=eng.launch_count())
         if st.stopped == _native.STOP_ERROR and st.err_code == _native.ERR_ZERO_COLUMN:
             raise ZeroDivisionError("a component of the accepted candidate has a zero-norm vector")
