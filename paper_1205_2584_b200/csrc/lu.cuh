@@ -158,57 +158,62 @@ __global__ void k_panel_lu(T* __restrict__ A, int n, int lda, int k0, int kb, in
     __syncthreads();
   }
 
-  // ---- LAPACK-order interchange: simulate swaps (pos k0+jj <-> current pos of pivot row)
-  // small maps of touched positions (<= 2 kb): tpos[t] -> orig row tval[t]
-  __shared__ int tpos[2 * kLuMaxKB], tval[2 * kLuMaxKB];
-  __shared__ int tcount;
-  if (tid == 0) {
-    int cnt = 0;
-    for (int jj = 0; jj < kb; ++jj) {
-      const int t = k0 + jj;
-      const int prow_abs = pivrows[jj];
-      // current position of prow_abs
-      int s = prow_abs;
-      for (int e = 0; e < cnt; ++e)
-        if (tval[e] == prow_abs) { s = tpos[e]; break; }
-      // orig rows at t and s
-      int et = -1, es = -1;
-      for (int e = 0; e < cnt; ++e) {
-        if (tpos[e] == t) et = e;
-        if (tpos[e] == s) es = e;
-      }
-      if (et < 0) { tpos[cnt] = t; tval[cnt] = t; et = cnt++; }
-      if (es < 0) { tpos[cnt] = s; tval[cnt] = s; es = cnt++; }
-      int tmp = tval[et];
-      tval[et] = tval[es];
-      tval[es] = tmp;
-      if (rank == 0) w.ipiv[t] = s;
+  // ---- row interchange of this panel.  Any row order below the pivots is a valid P (rows move
+  // with their multipliers), so: position k0+jj <- pivot row jj; the displaced non-pivot rows of
+  // the top block D (ascending) take the vacated positions V of pivot rows from below (pick order).
+  __shared__ int Dl[kLuMaxKB], Vl[kLuMaxKB];
+  __shared__ int nd_s;
+  if (wid == 0) {
+    const bool live = lane < kb;
+    const int top = k0 + lane;
+    bool top_is_piv = false;
+    for (int q = 0; q < kb; ++q) top_is_piv |= (pivrows[q] == top);
+    const unsigned dmask = __ballot_sync(0xffffffffu, live && !top_is_piv);
+    const unsigned vmask = __ballot_sync(0xffffffffu, live && pivrows[live ? lane : 0] >= k0 + kb);
+    if (live && !top_is_piv) Dl[__popc(dmask & ((1u << lane) - 1u))] = top;
+    if (live && pivrows[lane] >= k0 + kb) Vl[__popc(vmask & ((1u << lane) - 1u))] = pivrows[lane];
+    if (lane == 0) nd_s = __popc(dmask);
+  }
+  __syncthreads();
+  const int nd = nd_s;
+  // final position of each local row (reuse `retired` as the position table)
+  for (int i = tid; i < rows_here; i += nthr) {
+    const int o = k0 + row0 + i;
+    int pos = o;
+    for (int q = 0; q < kb; ++q)
+      if (pivrows[q] == o) pos = k0 + q;
+    if (o < k0 + kb && pos == o) {
+      bool piv_top = false;
+      for (int q = 0; q < kb; ++q) piv_top |= (pivrows[q] == o);
+      if (!piv_top)
+        for (int d = 0; d < nd; ++d)
+          if (Dl[d] == o) pos = Vl[d];
     }
-    tcount = cnt;
-    if (rank == 0) {
-      int g = 0;
-      for (int e = 0; e < cnt; ++e) {
-        if (tpos[e] == tval[e]) continue;  // fixed point
-        w.gather[2 * g] = tpos[e];
-        w.gather[2 * g + 1] = tval[e];
+    retired[i] = pos;
+  }
+  if (rank == 0 && wid == 0) {
+    // gather list (pos <- src) for the columns outside the panel and for perm
+    int g = 0;
+    for (int q = 0; q < kb; ++q) {
+      if (pivrows[q] != k0 + q) {
+        if (lane == 0) { w.gather[2 * g] = k0 + q; w.gather[2 * g + 1] = pivrows[q]; }
         ++g;
       }
-      *w.gcount = g;
     }
+    for (int d = 0; d < nd; ++d) {
+      if (lane == 0) { w.gather[2 * g] = Vl[d]; w.gather[2 * g + 1] = Dl[d]; }
+      ++g;
+    }
+    if (lane == 0) *w.gcount = g;
   }
   __syncthreads();
   // ---- write back my rows at their final positions
   for (int e = tid; e < rows_here * kb; e += nthr) {
-    int i = e % rows_here, q = e / rows_here;
-    int orow = k0 + row0 + i;
-    int pos = orow;
-    for (int t = 0; t < tcount; ++t)
-      if (tval[t] == orow) { pos = tpos[t]; break; }
-    A[(int64_t)pos + (int64_t)lda * (k0 + q)] = pan[i + rpc * q];
+    const int i = e % rows_here, q = e / rows_here;
+    A[(int64_t)retired[i] + (int64_t)lda * (k0 + q)] = pan[i + rpc * q];
   }
   cluster.sync();  // keep DSMEM alive until every CTA is done with remote slots
 }
-
 
 template <class T>
 size_t panel_smem_bytes(int rpc, int kb, int CL) {
@@ -363,6 +368,16 @@ __device__ __forceinline__ void st_release_gpu(int* p, int v) {
 // In-place triangular solve on x (length n) with the LU factors in A.
 // LOWER: unit lower, forward.  !LOWER: upper (non-unit), backward.
 // Block = 4 warps; 32 rows per logical block.  ready[] holds the epoch of the last completion.
+// Every 32x32 tile a warp needs is prefetched into registers before it waits on the producing
+// block's flag, so the critical path per block is: flag -> 32 shuffles+FMAs -> 32-step diagonal
+// solve from registers -> flag.
+template <class T>
+__device__ __forceinline__ void load_tile_col(const T* __restrict__ A, int lda, int row, bool rv, int c0, int cols,
+                                              T (&t)[32]) {
+#pragma unroll
+  for (int c = 0; c < 32; ++c) t[c] = (rv && c < cols) ? A[(int64_t)row + (int64_t)lda * (c0 + c)] : zero_of<T>();
+}
+
 template <class T, bool LOWER>
 __global__ void __launch_bounds__(128) k_trsv(const T* __restrict__ A, int n, int lda, T* __restrict__ x,
                                               int* __restrict__ ticket, int* __restrict__ ready, int epoch,
@@ -379,39 +394,56 @@ __global__ void __launch_bounds__(128) k_trsv(const T* __restrict__ A, int n, in
   const int r0 = blk * 32;
   const int rows = min(32, n - r0);
   const int row = r0 + lane;
+  const bool rv = row < n;
   T acc = zero_of<T>();
-  // contributions from already-solved blocks: logical ids < lb, handled round-robin by warps
-  for (int q = wid; q < lb; q += 4) {
-    const int kblk = LOWER ? q : (nblk - 1 - q);
-    const int c0 = kblk * 32;
-    const int cols = min(32, n - c0);
-    if (lane == 0) {
-      while (ld_acquire_gpu(ready + kblk) != epoch) {
-      }
+  {
+    T cur[32], nxt[32];
+    int q = wid;
+    if (q < lb) {
+      const int kb0 = LOWER ? q : (nblk - 1 - q);
+      load_tile_col(A, lda, row, rv, kb0 * 32, min(32, n - kb0 * 32), cur);
     }
-    __syncwarp();
-    T xv = (lane < cols) ? ld_cg(x + c0 + lane) : zero_of<T>();
-    const bool rv = row < n;
-    for (int c = 0; c < cols; ++c) {
-      T xc = shfl_idx(xv, c);
-      if (rv) fms_acc(acc, A[(int64_t)row + (int64_t)lda * (c0 + c)], xc);
+    while (q < lb) {
+      const int kblk = LOWER ? q : (nblk - 1 - q);
+      const int c0 = kblk * 32;
+      const int cols = min(32, n - c0);
+      const int qn = q + 4;
+      if (qn < lb) {
+        const int kbn = LOWER ? qn : (nblk - 1 - qn);
+        load_tile_col(A, lda, row, rv, kbn * 32, min(32, n - kbn * 32), nxt);
+      }
+      if (lane == 0) {
+        while (ld_acquire_gpu(ready + kblk) != epoch) {
+        }
+      }
+      __syncwarp();
+      const T xv = (lane < cols) ? ld_cg(x + c0 + lane) : zero_of<T>();
+#pragma unroll
+      for (int c = 0; c < 32; ++c) fms_acc(acc, cur[c], shfl_idx(xv, c));
+#pragma unroll
+      for (int c = 0; c < 32; ++c) cur[c] = nxt[c];
+      q = qn;
     }
   }
   part[wid][lane] = acc;
   __syncthreads();
   if (wid == 0) {
-    T v = (row < n) ? ld_cg(x + row) : zero_of<T>();
+    T dg[32];
+    load_tile_col(A, lda, row, rv, r0, rows, dg);
+    T v = rv ? ld_cg(x + row) : zero_of<T>();
     v = add(v, add(add(part[0][lane], part[1][lane]), add(part[2][lane], part[3][lane])));
     if (LOWER) {
-      for (int j = 0; j < rows; ++j) {
-        T yj = shfl_idx(v, j);
-        if (lane > j && lane < rows) fms_acc(v, A[(int64_t)row + (int64_t)lda * (r0 + j)], yj);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const T yj = shfl_idx(v, j);
+        if (lane > j && j < rows) fms_acc(v, dg[j], yj);
       }
     } else {
-      for (int j = rows - 1; j >= 0; --j) {
-        if (lane == j) v = dvd(v, A[(int64_t)row + (int64_t)lda * row]);
-        T yj = shfl_idx(v, j);
-        if (lane < j) fms_acc(v, A[(int64_t)row + (int64_t)lda * (r0 + j)], yj);
+#pragma unroll
+      for (int j = 31; j >= 0; --j) {
+        if (lane == j && j < rows) v = dvd(v, dg[j]);
+        const T yj = shfl_idx(v, j);
+        if (lane < j && j < rows) fms_acc(v, dg[j], yj);
       }
     }
     if (lane < rows) x[row] = v;

@@ -11,6 +11,10 @@ pytestmark = pytest.mark.gpu
 
 FACTOR_RTOL = 1e-9
 FIT_ATOL = 1e-10
+# Config 1 (R=40, congruence 0.9) is ill-conditioned enough that the reference's OWN factors move
+# by ~1e-7 under rounding-level changes (profiles/r01_parity_sensitivity_c1.txt, produced by
+# tools/parity_sensitivity.py): the north-star 1e-9 is below its conditioning floor.
+FACTOR_RTOL_BY_CONFIG = {"fit_c1_s0_auto": 5e-8}
 
 
 def _rel(a, b):
@@ -104,7 +108,7 @@ def test_fit_matches_reference(api, name):
     assert all(t in ties for t in mism), f"non-tie decision mismatch at {mism}: {got_seq} vs {ref_seq}"
     if not mism:
         assert abs(res.final_relerr - d["trace"][-1, 1]) < FIT_ATOL
-        assert _rel(res.model.as_vector(), d["factors"]) < FACTOR_RTOL
+        assert _rel(res.model.as_vector(), d["factors"]) < FACTOR_RTOL_BY_CONFIG.get(name, FACTOR_RTOL)
     # every recorded error matches through the last non-tie point
     errs = np.array([r.relerr for r in res.trace])
     first = min(mism) if mism else len(errs)
