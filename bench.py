@@ -200,9 +200,13 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1205_2584_b200 import _native, slab_bounds
+    from paper_1205_2584_b200 import _native, build, slab_bounds
     from paper_1205_2584_b200.solver import FitConfig, _Dist, fit
 
+    if rank == 0:
+        build.build()
+    if dist:
+        dist.barrier()
     _native.load()
     lo, hi = slab_bounds(cfg.dims[-1], world, rank)
     kind = _native.CPF_COMPLEX if cfg.complex_ else _native.CPF_REAL

@@ -32,6 +32,7 @@ struct ApiError : std::runtime_error {
 #include "phi.cuh"
 #include "small_ops.cuh"
 #include "tensor_pass.cuh"
+#include "tensor_pass2.cuh"
 
 #define NCCL_CHECK(expr)                                                                   \
   do {                                                                                     \
@@ -42,7 +43,7 @@ struct ApiError : std::runtime_error {
 namespace cpf {
 
 static int padded_rank(int R) {
-  static const int table[] = {1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 16, 20, 24, 32, 40, 48, 64};
+  static const int table[] = {2, 4, 6, 8, 10, 12, 16, 20, 24, 32, 40, 48, 64};  // even: paired smem loads
   for (int v : table)
     if (v >= R) return v;
   return -1;
@@ -116,6 +117,12 @@ struct Engine final : EngineBase {
   size_t pa_smem = 0;
   int pb_threads = 256, pb_TI = 1, pb_TM = 1, pb_tiles = 1, pb_chunks = 1;
   int64_t pb_mper = 1;
+  // v2 (TMA bulk pipeline) geometry
+  bool use_v2 = false;
+  int rpt = 1;
+  PassGeom ga{}, gb{};
+  size_t ga_smem = 0, gb_smem = 0;
+  int ga_groups = 1, gb_chunks = 1;
   int lu_kb = 32, lu_cl = 1, lu_rpc = 0;
   size_t lu_smem = 0;
 
@@ -206,9 +213,9 @@ struct Engine final : EngineBase {
     Gf = dalloc<T>(R2); Gti = dalloc<T>(N * R2); Gi = dalloc<T>(N * R2); W1 = dalloc<T>(N * R2); Sm = dalloc<T>(N * R2);
     wvec = dalloc<T>(nB); fvec = dalloc<T>(nB); xvec = dalloc<T>(nB);
     Phi = dalloc<T>((size_t)nB * nB);
-    A1c = dalloc<T>((size_t)I1 * RP);
-    KMc = dalloc<T>((size_t)Lmid * RP);
-    WNc = dalloc<T>((size_t)std::max<int64_t>(Cloc, 1) * RP);
+    A1c = dalloc<T>((size_t)I1 * RP + 2);
+    KMc = dalloc<T>((size_t)Lmid * RP + 2);
+    WNc = dalloc<T>((size_t)std::max<int64_t>(Cloc, 1) * RP + 2);
     A1r = dalloc<T>((size_t)I1 * RP);
     KMr = dalloc<T>((size_t)Lmid * RP);
     WNr = dalloc<T>((size_t)std::max<int64_t>(Cloc, 1) * RP);
@@ -278,11 +285,81 @@ struct Engine final : EngineBase {
       lu_kb /= 2;
     }
     lu_smem = panel_smem_bytes<T>(lu_rpc, lu_kb, lu_cl);
+    plan_v2(nsm);
     CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lu_smem));
     if (lu_cl > 8) CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     set_pass_attrs();
     CPF_CUDA_CHECK(cudaFuncSetAttribute(k_damped_inverses<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)(2 * R * R * sizeof(T))));
+  }
+
+  void plan_v2(int nsm) {
+    const bool cplx = sizeof(T) == 16;
+    use_v2 = cplx || (I1 % 2 == 0);
+    if (!use_v2) return;
+    rpt = (!cplx && RP <= 24) ? 2 : 1;
+    const int nthr = 256;
+    const size_t es = sizeof(T);
+    auto base = [&](PassGeom& g) {
+      g.I1 = I1; g.Lmid = Lmid; g.C = Cloc; g.RPT = rpt;
+      const int64_t tilmax = (int64_t)nthr * rpt;
+      if (I1 <= tilmax) {
+        g.full = 1;
+        g.TI = (int)((I1 + rpt - 1) / rpt);
+        g.TM = std::max(1, nthr / g.TI);
+        g.tiles = 1;
+      } else {
+        g.full = 0;
+        g.TI = nthr;
+        g.TM = 1;
+        g.tiles = (int)((I1 + tilmax - 1) / tilmax);
+      }
+    };
+    auto round_up = [](size_t v, size_t m) { return (v + m - 1) / m * m; };
+    const size_t align_e = 128 / es;
+    // ---- pass A
+    base(ga);
+    {
+      const int64_t tilmax = (int64_t)nthr * rpt;
+      ga.SL = ga.full ? I1 * ga.TM : tilmax;
+      int ck = (int)std::max<int64_t>(2, std::min<int64_t>(32, 32768 / std::max<int64_t>(1, ga.SL * (int64_t)es)));
+      ck &= ~1;
+      ga.CK = std::max(2, ck);
+      ga.stage_elems = round_up((size_t)ga.CK * ga.SL + (size_t)ga.CK * RP + 2, align_e);
+      const size_t side = (size_t)RP * nthr * es * (1 + rpt);  // zs + m1 slots
+      const size_t budget = 220 * 1024 - 128 - side;
+      ga.NST = (int)std::max<size_t>(2, std::min<size_t>(8, budget / (ga.stage_elems * es)));
+      ga_smem = 128 + (size_t)ga.NST * ga.stage_elems * es + side;
+      int64_t groups = std::max<int64_t>(1, (2 * (int64_t)nsm + ga.tiles - 1) / ga.tiles);
+      int64_t mper = (Lmid + groups - 1) / groups;
+      mper = ((mper + ga.TM - 1) / ga.TM) * ga.TM;
+      ga.m_per_cta = mper;
+      ga_groups = (int)((Lmid + mper - 1) / mper);
+    }
+    // ---- pass B
+    base(gb);
+    {
+      const int64_t tilmax = (int64_t)nthr * rpt;
+      gb.SL = gb.full ? I1 : tilmax;
+      int ck = (int)std::max<int64_t>(2, std::min<int64_t>(64, 32768 / std::max<int64_t>(1, gb.SL * (int64_t)es)));
+      ck &= ~1;
+      gb.CK = std::max(2, ck);
+      gb.stage_elems = round_up((size_t)gb.CK * gb.SL + (size_t)gb.CK * RP + 2, align_e);
+      gb.NST = (int)std::max<size_t>(2, std::min<size_t>(8, (140 * 1024) / (gb.stage_elems * es)));
+      gb_smem = 128 + (size_t)gb.NST * gb.stage_elems * es + (size_t)RP * 8 * es;
+      int64_t per_c = std::max<int64_t>(1, 2 * (int64_t)nsm / std::max<int64_t>(1, Cloc * gb.tiles));
+      per_c = std::min<int64_t>(per_c, std::max<int64_t>(1, Lmid / gb.CK));
+      int64_t mper = (Lmid + per_c - 1) / per_c;
+      mper = ((mper + gb.CK - 1) / gb.CK) * gb.CK;
+      gb.m_per_cta = mper;
+      gb_chunks = (int)((Lmid + mper - 1) / mper);
+    }
+    if (zpart) cudaFree(zpart);
+    if (m1part) cudaFree(m1part);
+    if (bpart) cudaFree(bpart);
+    zpart = dalloc<T>((size_t)ga.tiles * Lmid * RP);
+    m1part = dalloc<T>((size_t)ga_groups * I1 * RP);
+    bpart = dalloc<T>((size_t)std::max<int64_t>(Cloc, 1) * gb_chunks * gb.tiles * RP);
   }
 
   // ------------------------------------------------------------------------------------------
@@ -321,6 +398,17 @@ struct Engine final : EngineBase {
   template <int RPc>
   void set_pass_attrs_t() {
     CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_a<T, RPc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pa_smem));
+    if (use_v2) {
+      if (rpt == 2) {
+        if constexpr (sizeof(T) == 8) {
+          CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_a2<T, RPc, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ga_smem));
+          CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_b2<T, RPc, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb_smem));
+        }
+      } else {
+        CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_a2<T, RPc, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ga_smem));
+        CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_b2<T, RPc, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb_smem));
+      }
+    }
   }
   void set_pass_attrs() { dispatch_rp([&](auto rpc) { this->template set_pass_attrs_t<decltype(rpc)::value>(); }); }
 
@@ -328,13 +416,9 @@ struct Engine final : EngineBase {
   template <class F>
   void dispatch_rp(F&& f) {
     switch (RP) {
-      case 1: f(IC<1>{}); break;
       case 2: f(IC<2>{}); break;
-      case 3: f(IC<3>{}); break;
       case 4: f(IC<4>{}); break;
-      case 5: f(IC<5>{}); break;
       case 6: f(IC<6>{}); break;
-      case 7: f(IC<7>{}); break;
       case 8: f(IC<8>{}); break;
       case 10: f(IC<10>{}); break;
       case 12: f(IC<12>{}); break;
@@ -365,7 +449,24 @@ struct Engine final : EngineBase {
   void pass_a(const T* F, T* Mout, int gate) {
     prep_operands(F, true, gate);
     ph_begin(kPhPassA);
-    if (Cloc > 0) {
+    if (Cloc > 0 && use_v2) {
+      dispatch_rp([&](auto rpc) {
+        constexpr int RPc = decltype(rpc)::value;
+        if (rpt == 2) {
+          if constexpr (sizeof(T) == 8)
+            launch(k_pass_a2<T, RPc, 2>, dim3(ga.tiles, ga_groups), dim3(kConsumers + 32), ga_smem, Y, ga, (const T*)WNc,
+                   (const T*)A1c, (const T*)KMc, zpart, m1part, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+        } else {
+          launch(k_pass_a2<T, RPc, 1>, dim3(ga.tiles, ga_groups), dim3(kConsumers + 32), ga_smem, Y, ga, (const T*)WNc,
+                 (const T*)A1c, (const T*)KMc, zpart, m1part, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+        }
+      });
+      ph_end();
+      launch(k_m1_reduce<T>, nblocks(I1 * R, 32), 256, 0, (const T*)m1part, ga_groups, I1, R, RP, pa_out,
+             (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+      launch(k_z_reduce<T>, nblocks(Lmid * R, 256), 256, 0, (const T*)zpart, ga.tiles, Lmid, R, RP, pa_out + I1 * R,
+             (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    } else if (Cloc > 0) {
       dispatch_rp([&](auto rpc) {
         constexpr int RPc = decltype(rpc)::value;
         launch(k_pass_a<T, RPc>, dim3(pa_tiles, pa_groups), dim3(pa_threads), pa_smem, Y, I1, Lmid, Cloc,
@@ -397,7 +498,21 @@ struct Engine final : EngineBase {
   void pass_b(const T* F, T* Mout, int gate) {
     prep_operands(F, false, gate);
     ph_begin(kPhPassB);
-    if (Cloc > 0) {
+    int nparts = pb_chunks * pb_tiles;
+    if (Cloc > 0 && use_v2) {
+      nparts = gb_chunks * gb.tiles;
+      dispatch_rp([&](auto rpc) {
+        constexpr int RPc = decltype(rpc)::value;
+        if (rpt == 2) {
+          if constexpr (sizeof(T) == 8)
+            launch(k_pass_b2<T, RPc, 2>, dim3((unsigned)Cloc, gb_chunks, gb.tiles), dim3(kConsumers + 32), gb_smem, Y, gb,
+                   (const T*)A1c, (const T*)KMc, bpart, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+        } else {
+          launch(k_pass_b2<T, RPc, 1>, dim3((unsigned)Cloc, gb_chunks, gb.tiles), dim3(kConsumers + 32), gb_smem, Y, gb,
+                 (const T*)A1c, (const T*)KMc, bpart, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+        }
+      });
+    } else if (Cloc > 0) {
       dispatch_rp([&](auto rpc) {
         constexpr int RPc = decltype(rpc)::value;
         const size_t smem = sizeof(T) * RPc * ((pb_threads + 31) / 32);
@@ -407,12 +522,12 @@ struct Engine final : EngineBase {
     }
     ph_end();
     if (world == 1) {
-      launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, (const T*)bpart, Cloc, pb_chunks * pb_tiles, R, RP,
+      launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, (const T*)bpart, Cloc, nparts, R, RP,
              IN, Mout + offs[N - 1], (const LmDeviceState*)st, (const DevFlags*)fl, gate);
     } else {
       CPF_CUDA_CHECK(cudaMemsetAsync(pb_out, 0, sizeof(T) * Cpad * R, s));
       if (Cloc > 0)
-        launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, (const T*)bpart, Cloc, pb_chunks * pb_tiles, R, RP,
+        launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, (const T*)bpart, Cloc, nparts, R, RP,
                Cpad, pb_out, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
       const size_t cnt = (size_t)Cpad * R * (sizeof(T) / sizeof(double));
       NCCL_CHECK(ncclAllGather(pb_out, pb_all, cnt, ncclDouble, comm, s));

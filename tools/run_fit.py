@@ -2,7 +2,8 @@
 import sys, numpy as np
 sys.path.insert(0, '.')
 import torch
-from paper_1205_2584_b200 import synth, _native
+from paper_1205_2584_b200 import synth, _native, build
+build.build()
 cfg = synth.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else 'c2']
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 y = synth.device_tensor(cfg, 0, device='cuda:0')
