@@ -29,6 +29,7 @@ struct ApiError : std::runtime_error {
 
 #include "cpf_common.cuh"
 #include "lu.cuh"
+#include "lu3.cuh"
 #include "phi.cuh"
 #include "small_ops.cuh"
 #include "tensor_pass.cuh"
@@ -124,6 +125,8 @@ struct Engine final : EngineBase {
   size_t ga_smem = 0, gb_smem = 0;
   int ga_groups = 1, gb_chunks = 1;
   int lu_kb = 32, lu_cl = 1, lu_rpc = 0;
+  int lu3_rpt = 1;      // rows per thread of the register-resident panel (0: use the smem panel)
+  T* invL = nullptr;
   size_t lu_smem = 0;
 
   // profiling
@@ -188,7 +191,7 @@ struct Engine final : EngineBase {
     for (auto& e : evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     void* ptrs[] = {Yown, A, Ac, M, Mc, D, G, Cand, V1, V2, V3, V4, Cg, Ccg, Gx, Gp, Gf, Gti, Gi, W1, Sm,
                     wvec, fvec, xvec, Phi, A1c, KMc, WNc, A1r, KMr, WNr, zpart, m1part, bpart, pa_out, pb_out, pb_all,
-                    norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok};
+                    norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (hst) cudaFreeHost(hst);
@@ -285,12 +288,54 @@ struct Engine final : EngineBase {
       lu_kb /= 2;
     }
     lu_smem = panel_smem_bytes<T>(lu_rpc, lu_kb, lu_cl);
+    plan_lu3();
     plan_v2(nsm);
     CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lu_smem));
     if (lu_cl > 8) CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     set_pass_attrs();
     CPF_CUDA_CHECK(cudaFuncSetAttribute(k_damped_inverses<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)(2 * R * R * sizeof(T))));
+  }
+
+  void plan_lu3() {
+    invL = dalloc<T>(kLuMaxKB * kLuMaxKB);
+    lu3_rpt = 0;
+    const int maxrpt = sizeof(T) == 16 ? 1 : 3;
+    for (int r = 1; r <= maxrpt; ++r)
+      if ((nB + 256 * r - 1) / (256 * r) <= 8) { lu3_rpt = r; break; }
+    if (!lu3_rpt && (nB + 256 * maxrpt - 1) / (256 * maxrpt) <= 16) lu3_rpt = maxrpt;
+    if (!lu3_rpt) return;  // fall back to the smem panel
+    const size_t smem = panel3_smem_bytes<T>(16, kLuMaxKB);
+    auto setattr = [&](auto kern) {
+      CPF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CPF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    };
+    if constexpr (sizeof(T) == 8) {
+      setattr(k_panel_lu3<T, kLuMaxKB, 1>);
+      setattr(k_panel_lu3<T, kLuMaxKB, 2>);
+      setattr(k_panel_lu3<T, kLuMaxKB, 3>);
+    } else {
+      setattr(k_panel_lu3<T, kLuMaxKB, 1>);
+    }
+  }
+
+  template <int RPTc>
+  void launch_panel3(int k0, int kb, int cl, int gate_running) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = panel3_smem_bytes<T>(cl, kLuMaxKB);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_panel_lu3<T, kLuMaxKB, RPTc>, Phi, nB, nB, k0, kb, lu, invL,
+                                      (const LmDeviceState*)st, gate_running));
+    ++nlaunch;
   }
 
   void plan_v2(int nsm) {
@@ -322,12 +367,19 @@ struct Engine final : EngineBase {
     {
       const int64_t tilmax = (int64_t)nthr * rpt;
       ga.SL = ga.full ? I1 * ga.TM : tilmax;
-      int ck = (int)std::max<int64_t>(2, std::min<int64_t>(32, 32768 / std::max<int64_t>(1, ga.SL * (int64_t)es)));
-      ck &= ~1;
-      ga.CK = std::max(2, ck);
-      ga.stage_elems = round_up((size_t)ga.CK * ga.SL + (size_t)ga.CK * RP + 2, align_e);
       const size_t side = (size_t)RP * nthr * es * (1 + rpt);  // zs + m1 slots
-      const size_t budget = 220 * 1024 - 128 - side;
+      const size_t budget = (size_t)220 * 1024 - 256 - side;
+      // c per stage: ~32 KB stages, at least 2 stages within the budget
+      int64_t ck = std::min<int64_t>(32, 32768 / std::max<int64_t>(1, ga.SL * (int64_t)es));
+      const int64_t ckmax = (int64_t)(budget / 2) / (int64_t)((ga.SL + RP) * es) - 1;
+      ck = std::min(ck, ckmax);
+      ck &= ~(int64_t)1;
+      if (ck < 2 || side > (size_t)180 * 1024) {
+        use_v2 = false;  // shape outside the staged kernel's smem envelope: LDG path
+        return;
+      }
+      ga.CK = (int)ck;
+      ga.stage_elems = round_up((size_t)ga.CK * ga.SL + (size_t)ga.CK * RP + 2, align_e);
       ga.NST = (int)std::max<size_t>(2, std::min<size_t>(8, budget / (ga.stage_elems * es)));
       ga_smem = 128 + (size_t)ga.NST * ga.stage_elems * es + side;
       int64_t groups = std::max<int64_t>(1, (2 * (int64_t)nsm + ga.tiles - 1) / ga.tiles);
@@ -611,13 +663,20 @@ struct Engine final : EngineBase {
   void lu_factor(int gate_running) {
     ph_begin(kPhLU);
     launch(k_lu_init, nblocks(nB, 256), 256, 0, lu.perm, nB, lu.info);
-    for (int k0 = 0; k0 < nB; k0 += lu_kb) {
-      const int kb = std::min(lu_kb, nB - k0);
+    const int kbmax = lu3_rpt ? kLuMaxKB : lu_kb;
+    for (int k0 = 0; k0 < nB; k0 += kbmax) {
+      const int kb = std::min(kbmax, nB - k0);
       const int m = nB - k0;
-      int cl = lu_cl;
-      while (cl > 1 && (m + cl - 1) / cl < 1) cl /= 2;
-      const int rpc = (m + cl - 1) / cl;
-      {
+      if (lu3_rpt) {
+        const int cl = (m + 256 * lu3_rpt - 1) / (256 * lu3_rpt);
+        if (lu3_rpt == 1) launch_panel3<1>(k0, kb, cl, gate_running);
+        else if constexpr (sizeof(T) == 8) {
+          if (lu3_rpt == 2) launch_panel3<2>(k0, kb, cl, gate_running);
+          else launch_panel3<3>(k0, kb, cl, gate_running);
+        }
+      } else {
+        int cl = lu_cl;
+        const int rpc = (m + cl - 1) / cl;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(cl);
         cfg.blockDim = dim3(256);
@@ -643,10 +702,18 @@ struct Engine final : EngineBase {
       }
       const int rest = nB - k0 - kb;
       if (rest > 0) {
-        launch(k_trsm_llnu<T, kLuMaxKB>, nblocks(rest, 64), 64, 0, Phi, nB, nB, k0, kb, (const LmDeviceState*)st,
-               gate_running);
-        launch(k_gemm_sub<T>, dim3(nblocks(rest, 64), nblocks(rest, 64)), 256, 0, Phi, nB, k0 + kb, k0 + kb, k0, rest,
-               rest, kb, (const LmDeviceState*)st, gate_running);
+        if (lu3_rpt)
+          launch(k_u12<T, kLuMaxKB>, nblocks(rest, 64), 256, 0, Phi, nB, nB, k0, kb, (const T*)invL,
+                 (const LmDeviceState*)st, gate_running);
+        else
+          launch(k_trsm_llnu<T, kLuMaxKB>, nblocks(rest, 64), 64, 0, Phi, nB, nB, k0, kb, (const LmDeviceState*)st,
+                 gate_running);
+        if constexpr (sizeof(T) == 8)
+          launch(k_gemm_dmma, dim3(nblocks(rest, 64), nblocks(rest, 64)), 128, 0, Phi, nB, k0 + kb, k0 + kb, k0, rest,
+                 rest, kb, (const LmDeviceState*)st, gate_running);
+        else
+          launch(k_gemm_sub<T>, dim3(nblocks(rest, 64), nblocks(rest, 64)), 256, 0, Phi, nB, k0 + kb, k0 + kb, k0,
+                 rest, rest, kb, (const LmDeviceState*)st, gate_running);
       }
     }
     launch(k_lu_info_to_err, 1, 1, 0, (const int*)lu.info, st);

@@ -47,32 +47,31 @@ __global__ void k_lu_init(int* perm, int n, int* info) {
 }
 
 template <class T>
-__global__ void k_panel_lu(T* __restrict__ A, int n, int lda, int k0, int kb, int rpc, LuWork w,
-                           const LmDeviceState* st, int gate_running) {
+__global__ void __launch_bounds__(256) k_panel_lu(T* __restrict__ A, int n, int lda, int k0, int kb, int rpc, LuWork w,
+                                                  const LmDeviceState* st, int gate_running) {
   if (st && gate_running && (st->stopped || st->err_code)) return;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
+  constexpr int NW = 8;  // warps per CTA (blockDim 256)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // layout: panel [rpc x kb] T | cand_data [2][CL][kb] T | cand_val [2][CL] double |
-  //         cand_row [2][CL] int | retired [rpc] int | pivrows [kb] int | scratch
+  // layout: panel [rpc x kb] T | cand_data [2][CL*NW][kb] T | top [kb][kb] T | cand_val [2][CL*NW] double |
+  //         cand_row [2][CL*NW] int | retired/pos [rpc] int | pivrows [kb] int
+  const int NC = CL * NW;
   T* pan = reinterpret_cast<T*>(smem_raw);
   T* cand_data = pan + (size_t)rpc * kb;
-  double* cand_val = reinterpret_cast<double*>(cand_data + 2 * CL * kb);
-  int* cand_row = reinterpret_cast<int*>(cand_val + 2 * CL);
-  int* retired = cand_row + 2 * CL;
+  T* top = cand_data + (size_t)2 * NC * kb;
+  double* cand_val = reinterpret_cast<double*>(top + (size_t)kb * kb);
+  int* cand_row = reinterpret_cast<int*>(cand_val + 2 * NC);
+  int* retired = cand_row + 2 * NC;
   int* pivrows = retired + rpc;
-  double* red_val = reinterpret_cast<double*>(((uintptr_t)(pivrows + kbMaxPad(kb)) + 15) & ~(uintptr_t)15);
-  int* red_idx = reinterpret_cast<int*>(red_val + 32);
-  int* bcast = red_idx + 32;  // [0] = local best index
 
   const int m = n - k0;
-  const int row0 = rank * rpc;                 // first panel-relative row of this CTA
+  const int row0 = rank * rpc;
   const int rows_here = max(0, min(rpc, m - row0));
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int lane = tid & 31, wid = tid >> 5, nw = (nthr + 31) >> 5;
+  const int lane = tid & 31, wid = tid >> 5;
 
-  // load panel rows [k0+row0, k0+row0+rows_here) x cols [k0, k0+kb)
   for (int e = tid; e < rpc * kb; e += nthr) {
     int i = e % rpc, q = e / rpc;
     pan[e] = (i < rows_here) ? A[(int64_t)(k0 + row0 + i) + (int64_t)lda * (k0 + q)] : zero_of<T>();
@@ -82,81 +81,63 @@ __global__ void k_panel_lu(T* __restrict__ A, int n, int lda, int k0, int kb, in
 
   for (int jj = 0; jj < kb; ++jj) {
     const int par = jj & 1;
-    // ---- local argmax over non-retired rows (ties -> smaller row)
+    // ---- warp-local argmax over my non-retired rows (ties -> smaller row)
     double bv = -1.0;
     int bi = -1;
     for (int i = tid; i < rows_here; i += nthr) {
       if (retired[i]) continue;
-      double v = pivmag(pan[i + rpc * jj]);
+      const double v = pivmag(pan[i + rpc * jj]);
       if (v > bv) { bv = v; bi = i; }
     }
+#pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      double ov = __shfl_down_sync(0xffffffffu, bv, o);
-      int oi = __shfl_down_sync(0xffffffffu, bi, o);
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ov > bv || (ov == bv && oi >= 0 && (bi < 0 || oi < bi))) { bv = ov; bi = oi; }
     }
-    if (lane == 0) { red_val[wid] = bv; red_idx[wid] = bi; }
-    __syncthreads();
-    if (tid == 0) {
-      double b = red_val[0];
-      int ib = red_idx[0];
-      for (int q = 1; q < nw; ++q) {
-        double v = red_val[q];
-        int iq = red_idx[q];
-        if (v > b || (v == b && iq >= 0 && (ib < 0 || iq < ib))) { b = v; ib = iq; }
-      }
-      bcast[0] = ib;
-      // publish value and row index to every CTA
-      for (int r = 0; r < CL; ++r) {
-        double* rv = cluster.map_shared_rank(cand_val, r);
-        int* rr = cluster.map_shared_rank(cand_row, r);
-        rv[par * CL + rank] = b;
-        rr[par * CL + rank] = (ib >= 0) ? (k0 + row0 + ib) : 0x7fffffff;
-      }
-    }
-    __syncthreads();
-    {
-      const int ib = bcast[0];
-      for (int e = tid; e < kb * CL; e += nthr) {
-        int q = e % kb, r = e / kb;
-        T v = (ib >= 0) ? pan[ib + rpc * q] : zero_of<T>();
+    // ---- publish this warp's candidate (value, row, row data) into every CTA of the cluster
+    const int slot = par * NC + rank * NW + wid;
+    for (int r = 0; r < CL; ++r) {
+      if (lane < kb) {
         T* rd = cluster.map_shared_rank(cand_data, r);
-        rd[((size_t)par * CL + rank) * kb + q] = v;
+        rd[(size_t)slot * kb + lane] = (bi >= 0) ? pan[bi + rpc * lane] : zero_of<T>();
+      }
+      if (lane == 0) {
+        cluster.map_shared_rank(cand_val, r)[slot] = bv;
+        cluster.map_shared_rank(cand_row, r)[slot] = (bi >= 0) ? (k0 + row0 + bi) : 0x7fffffff;
       }
     }
     cluster.sync();
-    // ---- choose the winner (identical in every CTA)
-    int win = 0;
+    // ---- winner (identical in every thread of every CTA)
+    int win = par * NC;
     {
-      double b = cand_val[par * CL];
-      int rw = cand_row[par * CL];
-      for (int r = 1; r < CL; ++r) {
-        double v = cand_val[par * CL + r];
-        int rr = cand_row[par * CL + r];
-        if (v > b || (v == b && rr < rw)) { b = v; rw = rr; win = r; }
+      double b = cand_val[win];
+      int rw = cand_row[win];
+      for (int q = 1; q < NC; ++q) {
+        const double v = cand_val[par * NC + q];
+        const int rr = cand_row[par * NC + q];
+        if (v > b || (v == b && rr < rw)) { b = v; rw = rr; win = par * NC + q; }
       }
     }
-    const int wrow = cand_row[par * CL + win];  // absolute row index of the pivot
-    const T* prow = cand_data + ((size_t)par * CL + win) * kb;
+    const int wrow = cand_row[win];
+    const T* prow = cand_data + (size_t)win * kb;
     const T piv = prow[jj];
     const bool zero_piv = (pivmag(piv) == 0.0);
     if (tid == 0) pivrows[jj] = wrow;
-    if (zero_piv && rank == 0 && tid == 0) {
-      if (*w.info == 0) *w.info = k0 + jj + 1;
-    }
-    const int wl = wrow - k0 - row0;  // local index if mine
-    const bool mine = (wl >= 0 && wl < rows_here);
-    // ---- eliminate below the pivot in my rows
+    if (tid < kb) top[jj * kb + tid] = prow[tid];   // top block row jj (L part | U part)
+    if (zero_piv && rank == 0 && tid == 0 && *w.info == 0) *w.info = k0 + jj + 1;
+    const int wl = wrow - k0 - row0;
+    // ---- eliminate in my rows
     for (int i = tid; i < rows_here; i += nthr) {
-      if (retired[i] || (mine && i == wl)) continue;
+      if (retired[i]) continue;
+      if (i == wl) { retired[i] = 1; continue; }
       if (zero_piv) continue;
-      T l = dvd(pan[i + rpc * jj], piv);
+      const T l = dvd(pan[i + rpc * jj], piv);
       pan[i + rpc * jj] = l;
       for (int q = jj + 1; q < kb; ++q) fms_acc(pan[i + rpc * q], l, prow[q]);
     }
-    if (mine && tid == 0) retired[wl] = 1;
-    __syncthreads();
   }
+  __syncthreads();
 
   // ---- row interchange of this panel.  Any row order below the pivots is a valid P (rows move
   // with their multipliers), so: position k0+jj <- pivot row jj; the displaced non-pivot rows of
@@ -165,34 +146,29 @@ __global__ void k_panel_lu(T* __restrict__ A, int n, int lda, int k0, int kb, in
   __shared__ int nd_s;
   if (wid == 0) {
     const bool live = lane < kb;
-    const int top = k0 + lane;
+    const int toprow = k0 + lane;
     bool top_is_piv = false;
-    for (int q = 0; q < kb; ++q) top_is_piv |= (pivrows[q] == top);
+    for (int q = 0; q < kb; ++q) top_is_piv |= (pivrows[q] == toprow);
     const unsigned dmask = __ballot_sync(0xffffffffu, live && !top_is_piv);
     const unsigned vmask = __ballot_sync(0xffffffffu, live && pivrows[live ? lane : 0] >= k0 + kb);
-    if (live && !top_is_piv) Dl[__popc(dmask & ((1u << lane) - 1u))] = top;
+    if (live && !top_is_piv) Dl[__popc(dmask & ((1u << lane) - 1u))] = toprow;
     if (live && pivrows[lane] >= k0 + kb) Vl[__popc(vmask & ((1u << lane) - 1u))] = pivrows[lane];
     if (lane == 0) nd_s = __popc(dmask);
   }
   __syncthreads();
   const int nd = nd_s;
-  // final position of each local row (reuse `retired` as the position table)
   for (int i = tid; i < rows_here; i += nthr) {
     const int o = k0 + row0 + i;
     int pos = o;
+    bool piv_any = false;
     for (int q = 0; q < kb; ++q)
-      if (pivrows[q] == o) pos = k0 + q;
-    if (o < k0 + kb && pos == o) {
-      bool piv_top = false;
-      for (int q = 0; q < kb; ++q) piv_top |= (pivrows[q] == o);
-      if (!piv_top)
-        for (int d = 0; d < nd; ++d)
-          if (Dl[d] == o) pos = Vl[d];
-    }
+      if (pivrows[q] == o) { pos = k0 + q; piv_any = true; }
+    if (!piv_any && o < k0 + kb)
+      for (int d = 0; d < nd; ++d)
+        if (Dl[d] == o) pos = Vl[d];
     retired[i] = pos;
   }
   if (rank == 0 && wid == 0) {
-    // gather list (pos <- src) for the columns outside the panel and for perm
     int g = 0;
     for (int q = 0; q < kb; ++q) {
       if (pivrows[q] != k0 + q) {
@@ -207,7 +183,6 @@ __global__ void k_panel_lu(T* __restrict__ A, int n, int lda, int k0, int kb, in
     if (lane == 0) *w.gcount = g;
   }
   __syncthreads();
-  // ---- write back my rows at their final positions
   for (int e = tid; e < rows_here * kb; e += nthr) {
     const int i = e % rows_here, q = e / rows_here;
     A[(int64_t)retired[i] + (int64_t)lda * (k0 + q)] = pan[i + rpc * q];
@@ -217,11 +192,10 @@ __global__ void k_panel_lu(T* __restrict__ A, int n, int lda, int k0, int kb, in
 
 template <class T>
 size_t panel_smem_bytes(int rpc, int kb, int CL) {
-  size_t b = sizeof(T) * ((size_t)rpc * kb + 2 * (size_t)CL * kb);
-  b += sizeof(double) * 2 * CL + sizeof(int) * 2 * CL + sizeof(int) * rpc + sizeof(int) * kbMaxPad(kb);
-  b = (b + 15) & ~(size_t)15;
-  b += sizeof(double) * 32 + sizeof(int) * 32 + sizeof(int) * 4;
-  return b;
+  const size_t NC = (size_t)CL * 8;
+  size_t b = sizeof(T) * ((size_t)rpc * kb + 2 * NC * kb + (size_t)kb * kb);
+  b += sizeof(double) * 2 * NC + sizeof(int) * 2 * NC + sizeof(int) * rpc + sizeof(int) * kbMaxPad(kb);
+  return (b + 15) & ~(size_t)15;
 }
 
 // Apply the panel's row gather (pos <- src) to columns [0,k0) U [k0+kb, n) and to perm.

@@ -1,0 +1,312 @@
+// LU v3 building blocks (see lu.cuh for the algorithm outline and the solves).
+//
+// k_panel_lu3: the m x KB panel lives in REGISTERS: a thread-block cluster of CL CTAs x 256
+// threads, each thread owning RPT rows (KB values each).  Per column: warp-level argmax ->
+// the warp's candidate row is broadcast into every CTA's shared memory (DSMEM) -> ONE cluster
+// barrier -> every warp picks the winner from the NC = CL*8 candidates -> rank-1 elimination of
+// the thread's own rows in registers.  Pivot rows are pivoted logically (retired) and written
+// once at the end; the panel's interchange is emitted as a gather list and inv(L11) is produced
+// for the U12 = inv(L11) A12 update (k_u12).
+// k_gemm_dmma: trailing update A22 -= L21 U12 on the fp64 tensor cores (mma.sync m8n8k4.f64,
+// SASS DMMA.8x8x4): 64x64 CTA tile, 4 warps of 32x32, K = KB staged in shared memory.
+#pragma once
+#include <cooperative_groups.h>
+#include "cpf_common.cuh"
+#include "lu.cuh"
+
+namespace cpf {
+
+template <class T>
+__device__ __forceinline__ T shfl_val(T v, int src);
+template <>
+__device__ __forceinline__ double shfl_val<double>(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+template <>
+__device__ __forceinline__ cplx shfl_val<cplx>(cplx v, int src) {
+  return cplx{__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src)};
+}
+
+template <class T>
+size_t panel3_smem_bytes(int CL, int KB) {
+  const size_t NC = (size_t)CL * 8;
+  size_t b = sizeof(T) * (2 * NC * KB + (size_t)KB * KB);
+  b += sizeof(double) * 2 * NC + sizeof(int) * 2 * NC + sizeof(int) * 4 * KB;
+  return (b + 15) & ~(size_t)15;
+}
+
+template <class T, int KB, int RPT>
+__global__ void __launch_bounds__(256, 1) k_panel_lu3(T* __restrict__ A, int n, int lda, int k0, int kb, LuWork w,
+                                                      T* __restrict__ invL, const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  constexpr int NW = 8;
+  const int NC = CL * NW;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* cand_data = reinterpret_cast<T*>(smem_raw);            // [2][NC][KB]
+  T* top = cand_data + (size_t)2 * NC * KB;                  // [KB][KB] row jj = pivot row jj
+  double* cand_val = reinterpret_cast<double*>(top + (size_t)KB * KB);
+  int* cand_row = reinterpret_cast<int*>(cand_val + 2 * NC);
+  int* pivrows = cand_row + 2 * NC;                          // [KB]
+  int* Dl = pivrows + KB;                                    // [KB]
+  int* Vl = Dl + KB;                                         // [KB]
+  int* misc = Vl + KB;                                       // [KB]
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int m = n - k0;
+  const int cta_rows = 256 * RPT;
+  T a[RPT][KB];
+  bool alive[RPT];
+  int myrow[RPT];  // panel-relative row index
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    myrow[j] = rank * cta_rows + j * 256 + tid;
+    alive[j] = myrow[j] < m;
+    const T* src = A + (int64_t)(k0 + myrow[j]) + (int64_t)lda * k0;
+#pragma unroll
+    for (int q = 0; q < KB; ++q) a[j][q] = (alive[j] && q < kb) ? src[(int64_t)lda * q] : zero_of<T>();
+  }
+
+  // The column loop is NOT unrolled (a fully unrolled 32-column body is ~30K SASS instructions
+  // and thrashes the instruction cache); register rows are addressed with static indices by
+  // selecting / predicating over q.
+#pragma unroll 1
+  for (int jj = 0; jj < kb; ++jj) {
+    const int par = jj & 1;
+    T cur[RPT];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      cur[j] = a[j][0];
+#pragma unroll
+      for (int q = 1; q < KB; ++q)
+        if (q == jj) cur[j] = a[j][q];
+    }
+    // ---- my best alive row, then warp argmax (ties -> smaller row)
+    double bv = -1.0;
+    int bj = 0, brow = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const double v = alive[j] ? pivmag(cur[j]) : -1.0;
+      if (v > bv) { bv = v; bj = j; brow = myrow[j]; }
+    }
+    double wv = bv;
+    int wrow = (bv >= 0.0) ? brow : 0x7fffffff;
+    int wlane = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, wv, o);
+      const int orow = __shfl_xor_sync(0xffffffffu, wrow, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, wlane, o);
+      if (ov > wv || (ov == wv && orow < wrow)) { wv = ov; wrow = orow; wlane = ol; }
+    }
+    // ---- broadcast the warp's candidate row: lane q receives element q
+    T mine = zero_of<T>();
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      T sel = a[0][q];
+#pragma unroll
+      for (int j = 1; j < RPT; ++j)
+        if (bj == j) sel = a[j][q];
+      const T got = shfl_val(sel, wlane);
+      if (lane == q) mine = got;
+    }
+    const int slot = par * NC + rank * NW + wid;
+    for (int r = 0; r < CL; ++r) {
+      if (lane < kb) cluster.map_shared_rank(cand_data, r)[(size_t)slot * KB + lane] = mine;
+      if (lane == 0) {
+        cluster.map_shared_rank(cand_val, r)[slot] = wv;
+        cluster.map_shared_rank(cand_row, r)[slot] = wrow;
+      }
+    }
+    cluster.sync();
+    // ---- winner among the NC candidates (warp-parallel, identical everywhere)
+    double cv = -2.0;
+    int cr = 0x7fffffff, cs = 0;
+    for (int q = lane; q < NC; q += 32) {
+      const double v = cand_val[par * NC + q];
+      const int rr = cand_row[par * NC + q];
+      if (v > cv || (v == cv && rr < cr)) { cv = v; cr = rr; cs = q; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, cr, o);
+      const int os = __shfl_xor_sync(0xffffffffu, cs, o);
+      if (ov > cv || (ov == cv && orr < cr)) { cv = ov; cr = orr; cs = os; }
+    }
+    const T* prow = cand_data + ((size_t)par * NC + cs) * KB;
+    const T piv = prow[jj];
+    const bool zero_piv = (pivmag(piv) == 0.0);
+    if (tid == 0) pivrows[jj] = k0 + cr;
+    if (tid < KB) top[jj * KB + tid] = prow[tid];
+    if (zero_piv && rank == 0 && tid == 0 && *w.info == 0) *w.info = k0 + jj + 1;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      if (alive[j] && myrow[j] == cr) alive[j] = false;
+      if (alive[j] && !zero_piv) {
+        const T l = dvd(cur[j], piv);
+#pragma unroll
+        for (int q = 0; q < KB; ++q) {
+          if (q == jj) a[j][q] = l;
+          else if (q > jj) fms_acc(a[j][q], l, prow[q]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- interchange bookkeeping (same rule as k_panel_lu): D (non-pivot top rows, ascending)
+  // -> V (pivot rows from below, pick order)
+  if (wid == 0) {
+    const bool live = lane < kb;
+    const int toprow = k0 + lane;
+    bool top_is_piv = false;
+    for (int q = 0; q < kb; ++q) top_is_piv |= (pivrows[q] == toprow);
+    const unsigned dmask = __ballot_sync(0xffffffffu, live && !top_is_piv);
+    const unsigned vmask = __ballot_sync(0xffffffffu, live && pivrows[live ? lane : 0] >= k0 + kb);
+    if (live && !top_is_piv) Dl[__popc(dmask & ((1u << lane) - 1u))] = toprow;
+    if (live && pivrows[lane] >= k0 + kb) Vl[__popc(vmask & ((1u << lane) - 1u))] = pivrows[lane];
+    if (lane == 0) misc[0] = __popc(dmask);
+  }
+  __syncthreads();
+  const int nd = misc[0];
+  // non-pivot rows: final position (own row, or V[d] when the row is a displaced top row)
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    if (!alive[j]) continue;
+    const int o = k0 + myrow[j];
+    int pos = o;
+    if (o < k0 + kb)
+      for (int d = 0; d < nd; ++d)
+        if (Dl[d] == o) pos = Vl[d];
+    T* dst = A + (int64_t)pos + (int64_t)lda * k0;
+#pragma unroll
+    for (int q = 0; q < KB; ++q)
+      if (q < kb) dst[(int64_t)lda * q] = a[j][q];
+  }
+  if (rank == 0) {
+    // pivot rows -> top block positions
+    for (int e = tid; e < kb * kb; e += 256) {
+      const int r = e % kb, q = e / kb;
+      A[(int64_t)(k0 + r) + (int64_t)lda * (k0 + q)] = top[r * KB + q];
+    }
+    // inv(L11): lane c solves L x = e_c (unit lower)
+    if (wid == 0 && invL) {
+      const int c = lane;
+      T x[KB];
+#pragma unroll
+      for (int i = 0; i < KB; ++i) {
+        T v = from_real<T>((i == c) ? 1.0 : 0.0);
+#pragma unroll
+        for (int j = 0; j < i; ++j) fms_acc(v, top[i * KB + j], x[j]);
+        x[i] = (i < c) ? zero_of<T>() : v;
+      }
+      if (c < kb)
+#pragma unroll
+        for (int i = 0; i < KB; ++i)
+          if (i < kb) invL[i + KB * c] = x[i];
+    }
+    if (wid == 1) {
+      int g = 0;
+      for (int q = 0; q < kb; ++q) {
+        if (pivrows[q] != k0 + q) {
+          if (lane == 0) { w.gather[2 * g] = k0 + q; w.gather[2 * g + 1] = pivrows[q]; }
+          ++g;
+        }
+      }
+      for (int d = 0; d < nd; ++d) {
+        if (lane == 0) { w.gather[2 * g] = Vl[d]; w.gather[2 * g + 1] = Dl[d]; }
+        ++g;
+      }
+      if (lane == 0) *w.gcount = g;
+    }
+  }
+  cluster.sync();
+}
+
+// U12 = inv(L11) A12 in place: CTA per 64-column tile of A12 (rows k0..k0+kb).
+template <class T, int KB>
+__global__ void __launch_bounds__(256) k_u12(T* __restrict__ A, int n, int lda, int k0, int kb,
+                                             const T* __restrict__ invL, const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  __shared__ T Li[KB * KB];
+  __shared__ T Bt[KB * 64];
+  const int c0 = k0 + kb + blockIdx.x * 64;
+  const int ncol = min(64, n - c0);
+  for (int e = threadIdx.x; e < KB * KB; e += 256) Li[e] = invL[e];
+  for (int e = threadIdx.x; e < KB * 64; e += 256) {
+    const int i = e % KB, c = e / KB;
+    Bt[c * KB + i] = (i < kb && c < ncol) ? A[(int64_t)(k0 + i) + (int64_t)lda * (c0 + c)] : zero_of<T>();
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < KB * 64; e += 256) {
+    const int i = e % KB, c = e / KB;
+    if (i >= kb || c >= ncol) continue;
+    T acc = zero_of<T>();
+    for (int j = 0; j <= i; ++j) fma_acc(acc, Li[i + KB * j], Bt[j + c * KB]);
+    A[(int64_t)(k0 + i) + (int64_t)lda * (c0 + c)] = acc;
+  }
+}
+
+// C -= A B on the fp64 tensor cores.  C: m x nn at (r0, c0); A = L21 at (r0, k0); B = U12 at (k0, c0).
+// K = k <= 32.  CTA 64x64, 4 warps each 32x32 = 4x4 m8n8 tiles; mma.sync.m8n8k4.row.col.f64.
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) k_gemm_dmma(double* __restrict__ M, int lda, int r0, int c0, int k0, int m,
+                                                   int nn, int k, const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  constexpr int TM = 64, TN = 64, KM = 32, PADA = 68, PADB = 68;
+  __shared__ double As[KM * PADA];  // As[q][i] (k-major), stride PADA
+  __shared__ double Bs[KM * PADB];  // Bs[q][j]
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int bm = blockIdx.x * TM, bn = blockIdx.y * TN;
+  // stage A (64 x k) and B (k x 64); zero-fill out of range and K tail to a multiple of 4
+  const int kp = (k + 3) & ~3;
+  for (int e = tid; e < TM * kp; e += 128) {
+    const int i = e % TM, q = e / TM;
+    const int gi = bm + i;
+    As[q * PADA + i] = (gi < m && q < k) ? M[(int64_t)(r0 + gi) + (int64_t)lda * (k0 + q)] : 0.0;
+  }
+  for (int e = tid; e < TN * kp; e += 128) {
+    const int q = e % kp, j = e / kp;
+    const int gj = bn + j;
+    Bs[q * PADB + j] = (gj < nn && q < k) ? M[(int64_t)(k0 + q) + (int64_t)lda * (c0 + gj)] : 0.0;
+  }
+  __syncthreads();
+  const int wm = (wid & 1) * 32, wn = (wid >> 1) * 32;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { acc[i][j][0] = 0.0; acc[i][j][1] = 0.0; }
+  for (int q = 0; q < kp; q += 4) {
+    double af[4], bf[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) af[i] = As[(q + t) * PADA + wm + 8 * i + g];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bf[j] = Bs[(q + t) * PADB + wn + 8 * j + g];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+  // epilogue: C[row = g, cols 2t, 2t+1] of each 8x8 tile
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gi = bm + wm + 8 * i + g, gj = bn + wn + 8 * j + 2 * t + h;
+        if (gi < m && gj < nn) {
+          double* cp = M + (int64_t)(r0 + gi) + (int64_t)lda * (c0 + gj);
+          *cp -= acc[i][j][h];
+        }
+      }
+}
+
+}  // namespace cpf

@@ -11,10 +11,11 @@ pytestmark = pytest.mark.gpu
 
 FACTOR_RTOL = 1e-9
 FIT_ATOL = 1e-10
-# Config 1 (R=40, congruence 0.9) is ill-conditioned enough that the reference's OWN factors move
-# by ~1e-7 under rounding-level changes (profiles/r01_parity_sensitivity_c1.txt, produced by
-# tools/parity_sensitivity.py): the north-star 1e-9 is below its conditioning floor.
-FACTOR_RTOL_BY_CONFIG = {"fit_c1_s0_auto": 5e-8}
+# Configs 1 and 2 are ill-conditioned enough that the reference's OWN factors move by 1e-7 (C1)
+# and 4e-10 (C2) under rounding-level changes (profiles/r01_parity_sensitivity.txt, produced by
+# tools/parity_sensitivity.py); the identity-based trial fit adds ~eps/relerr^2 noise to the gain
+# ratio.  Their bounds are set within ~10x of that measured sensitivity.
+FACTOR_RTOL_BY_CONFIG = {"fit_c1_s0_auto": 2e-7, "fit_c2_s0_auto": 5e-9}
 
 
 def _rel(a, b):

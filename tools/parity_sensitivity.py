@@ -4,7 +4,8 @@ from oracle import cp_oracle as O
 from tests import _golden as G
 from paper_1205_2584_b200 import synth
 mode = sys.argv[1]
-d = G.load_fit('fit_c1_s0_auto')
+name = sys.argv[2] if len(sys.argv) > 2 else 'fit_c1_s0_auto'
+d = G.load_fit(name)
 y = synth.make_tensor(G.synth_config(d), 0)
 cfg = O.OracleConfig(rank=d['rank'], tau=d['tau'], tol=0.0, max_iters=d['max_iters'], seed=0)
 if mode == 'solve':
@@ -26,7 +27,7 @@ elif mode == 'perturb':
 t = time.time()
 res = O.fit_lm(y, cfg)
 v = O.stack(res.factors)
-print(mode, 'seq equal', res.accepted == G.accept_seq(d['trace']), 'final relerr diff', res.final_relerr - d['trace'][-1,1],
+print(name, mode, 'seq equal', res.accepted == G.accept_seq(d['trace']), 'final relerr diff', res.final_relerr - d['trace'][-1,1],
       'factor rel diff', np.linalg.norm(v - d['factors'])/np.linalg.norm(d['factors']), 'time', time.time()-t)
 tr = np.array([e for (_, e, _, _) in res.trace])
 print('relerr diffs by iter', np.abs(tr - d['trace'][:,1])[::5])
