@@ -34,6 +34,7 @@ struct ApiError : std::runtime_error {
 #include "small_ops.cuh"
 #include "tensor_pass.cuh"
 #include "tensor_pass2.cuh"
+#include "tensor_pass_dmma.cuh"
 
 #define NCCL_CHECK(expr)                                                                   \
   do {                                                                                     \
@@ -118,6 +119,13 @@ struct Engine final : EngineBase {
   size_t pa_smem = 0;
   int pb_threads = 256, pb_TI = 1, pb_TM = 1, pb_tiles = 1, pb_chunks = 1;
   int64_t pb_mper = 1;
+  // DMMA (fp64 tensor core) passes for float64 with large I1
+  bool use_dmma = false;
+  int dm_nt = 0;
+  DmmaGeom da{}, db{};
+  size_t da_smem = 0, db_smem = 0;
+  int da_groups = 1, db_chunks = 1;
+  double *WNd = nullptr, *KMd = nullptr;
   // v2 (TMA bulk pipeline) geometry
   bool use_v2 = false;
   int rpt = 1;
@@ -191,7 +199,7 @@ struct Engine final : EngineBase {
     for (auto& e : evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     void* ptrs[] = {Yown, A, Ac, M, Mc, D, G, Cand, V1, V2, V3, V4, Cg, Ccg, Gx, Gp, Gf, Gti, Gi, W1, Sm,
                     wvec, fvec, xvec, Phi, A1c, KMc, WNc, A1r, KMr, WNr, zpart, m1part, bpart, pa_out, pb_out, pb_all,
-                    norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL};
+                    norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL, WNd, KMd};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (hst) cudaFreeHost(hst);
@@ -290,6 +298,7 @@ struct Engine final : EngineBase {
     lu_smem = panel_smem_bytes<T>(lu_rpc, lu_kb, lu_cl);
     plan_lu3();
     plan_v2(nsm);
+    plan_dmma(nsm);
     CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lu_smem));
     if (lu_cl > 8) CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     set_pass_attrs();
@@ -336,6 +345,73 @@ struct Engine final : EngineBase {
     CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_panel_lu3<T, kLuMaxKB, RPTc>, Phi, nB, nB, k0, kb, lu, invL,
                                       (const LmDeviceState*)st, gate_running));
     ++nlaunch;
+  }
+
+  template <int NT>
+  void set_dmma_attrs() {
+    CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_dmma<NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)da_smem));
+    CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_dmma<NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)db_smem));
+  }
+  template <class F>
+  void dispatch_nt(F&& f) {
+    switch (dm_nt) {
+      case 1: f(IC<1>{}); break;
+      case 2: f(IC<2>{}); break;
+      case 3: f(IC<3>{}); break;
+      case 4: f(IC<4>{}); break;
+      case 5: f(IC<5>{}); break;
+      case 6: f(IC<6>{}); break;
+      case 8: f(IC<8>{}); break;
+      default: throw ApiError(CPF_E_UNSUPPORTED, "unsupported DMMA n-tile count");
+    }
+  }
+
+  void plan_dmma(int nsm) {
+    use_dmma = false;
+    if constexpr (sizeof(T) != 8) return;
+    else {
+      if (I1 < 256 || I1 % 2 != 0 || Cloc < 1) return;
+      if (const char* e = getenv("CPF_NO_DMMA")) if (e[0] == '1') return;
+      dm_nt = (R + 7) / 8;
+      if (dm_nt == 7) dm_nt = 8;
+      int ws = 8 * dm_nt;
+      while (ws % 16 != 4) ++ws;
+      auto fill = [&](DmmaGeom& g) {
+        g.I1 = I1; g.Lmid = Lmid; g.C = Cloc; g.WS = ws;
+        g.tiles = (int)((I1 + kDmmaRows - 1) / kDmmaRows);
+        g.CK = 8;
+        g.stage_elems = ((size_t)g.CK * (kDmmaSLp + ws) + 15) / 16 * 16;
+      };
+      fill(da);
+      fill(db);
+      const size_t sb = da.stage_elems * sizeof(double);
+      const size_t m1b = (size_t)8 * 8 * dm_nt * 2 * 32 * sizeof(double);
+      const size_t redb = (size_t)8 * 8 * dm_nt * sizeof(double);
+      const size_t budget = (size_t)220 * 1024 - 128;
+      if (m1b + redb + 2 * sb > budget) return;
+      da.NST = (int)std::min<size_t>(6, (budget - m1b - redb) / sb);
+      db.NST = (int)std::min<size_t>(6, (budget - redb) / sb);
+      da_smem = 128 + (size_t)da.NST * sb + m1b + redb;
+      db_smem = 128 + (size_t)db.NST * sb + redb;
+      int64_t groups = std::max<int64_t>(1, ((int64_t)nsm + da.tiles - 1) / da.tiles);
+      groups = std::min<int64_t>(groups, Lmid);
+      da.m_per_cta = (Lmid + groups - 1) / groups;
+      da_groups = (int)((Lmid + da.m_per_cta - 1) / da.m_per_cta);
+      int64_t per_c = std::max<int64_t>(1, 2 * (int64_t)nsm / std::max<int64_t>(1, Cloc * db.tiles));
+      per_c = std::min<int64_t>(per_c, std::max<int64_t>(1, Lmid / 64));
+      db.m_per_cta = (Lmid + per_c - 1) / per_c;
+      db_chunks = (int)((Lmid + db.m_per_cta - 1) / db.m_per_cta);
+      WNd = dalloc<double>((size_t)Cloc * ws + 8);
+      KMd = dalloc<double>((size_t)Lmid * ws + 8);
+      if (zpart) cudaFree(zpart);
+      if (m1part) cudaFree(m1part);
+      if (bpart) cudaFree(bpart);
+      zpart = dalloc<T>((size_t)da.tiles * Lmid * RP);
+      m1part = dalloc<T>((size_t)std::max(da_groups, 1) * I1 * RP + (size_t)Cloc * db_chunks * db.tiles * RP);
+      bpart = dalloc<T>((size_t)std::max<int64_t>(Cloc, 1) * db_chunks * db.tiles * RP);
+      dispatch_nt([&](auto ntc) { this->template set_dmma_attrs<decltype(ntc)::value>(); });
+      use_dmma = true;
+    }
   }
 
   void plan_v2(int nsm) {
@@ -501,6 +577,26 @@ struct Engine final : EngineBase {
   void pass_a(const T* F, T* Mout, int gate) {
     prep_operands(F, true, gate);
     ph_begin(kPhPassA);
+    if constexpr (sizeof(T) == 8) {
+      if (Cloc > 0 && use_dmma) {
+        const LmDeviceState* cst = st;
+        const DevFlags* cfl = fl;
+        launch(k_conj_rowmajor<T>, nblocks(Cloc * da.WS, 256), 256, 0, (const T*)(F + offs[N - 1]), Cloc, slab_lo, IN, R,
+               da.WS, (T*)WNd, cst, cfl, gate, 1);
+        dispatch_nt([&](auto ntc) {
+          constexpr int NTc = decltype(ntc)::value;
+          launch(k_pass_dmma<NTc, 0>, dim3(da.tiles, da_groups), dim3(kConsumers + 32), da_smem, (const double*)Y, da,
+                 (const double*)WNd, (const double*)A1c, (const double*)KMc, RP, R, (double*)zpart, (double*)m1part,
+                 cst, cfl, gate);
+        });
+        ph_end();
+        launch(k_m1_reduce<T>, nblocks(I1 * R, 32), 256, 0, (const T*)m1part, da_groups, I1, R, RP, pa_out, cst, cfl,
+               gate);
+        launch(k_z_reduce<T>, nblocks(Lmid * R, 256), 256, 0, (const T*)zpart, da.tiles, Lmid, R, RP, pa_out + I1 * R,
+               cst, cfl, gate);
+        goto pass_a_done;
+      }
+    }
     if (Cloc > 0 && use_v2) {
       dispatch_rp([&](auto rpc) {
         constexpr int RPc = decltype(rpc)::value;
@@ -531,6 +627,7 @@ struct Engine final : EngineBase {
       ph_end();
       CPF_CUDA_CHECK(cudaMemsetAsync(pa_out, 0, sizeof(T) * (I1 + Lmid) * R, s));
     }
+  pass_a_done:
     if (world > 1) {
       NCCL_CHECK(ncclAllReduce(pa_out, pa_out, (size_t)(I1 + Lmid) * R * (sizeof(T) / sizeof(double)), ncclDouble,
                                ncclSum, comm, s));
@@ -551,7 +648,28 @@ struct Engine final : EngineBase {
     prep_operands(F, false, gate);
     ph_begin(kPhPassB);
     int nparts = pb_chunks * pb_tiles;
-    if (Cloc > 0 && use_v2) {
+    bool done_b = false;
+    if constexpr (sizeof(T) == 8) {
+      if (Cloc > 0 && use_dmma) {
+        const LmDeviceState* cst = st;
+        const DevFlags* cfl = fl;
+        nparts = db_chunks * db.tiles;
+        if (N == 3)
+          launch(k_conj_rowmajor<T>, nblocks(Lmid * db.WS, 256), 256, 0, (const T*)(F + offs[1]), Lmid, (int64_t)0, Lmid,
+                 R, db.WS, (T*)KMd, cst, cfl, gate, 1);
+        else
+          launch(k_krmid<T>, nblocks(Lmid * db.WS, 256), 256, 0, F, mg, Lmid, R, db.WS, (T*)KMd, cst, cfl, gate, 1);
+        dispatch_nt([&](auto ntc) {
+          constexpr int NTc = decltype(ntc)::value;
+          launch(k_pass_dmma<NTc, 1>, dim3(db.tiles, (unsigned)Cloc, db_chunks), dim3(kConsumers + 32), db_smem,
+                 (const double*)Y, db, (const double*)KMd, (const double*)A1c, (const double*)KMc, RP, R, (double*)zpart,
+                 (double*)bpart, cst, cfl, gate);
+        });
+        done_b = true;
+      }
+    }
+    if (done_b) {
+    } else if (Cloc > 0 && use_v2) {
       nparts = gb_chunks * gb.tiles;
       dispatch_rp([&](auto rpc) {
         constexpr int RPc = decltype(rpc)::value;

@@ -164,3 +164,35 @@ def test_flm_b_singular_kernel_is_error_stop(api):
     model = api.KruskalModel(fac)
     with pytest.raises(api.SingularKernelError):
         api.flm_step(y, model, 0.1, "flm-b")
+
+
+# ---- shapes that take the fp64 tensor-core (DMMA) pass path (float64, I1 >= 256) and the
+# ---- 2-row-tiled DFMA path, checked against the live oracle
+@pytest.mark.parametrize("dims,rank", [((600, 7, 9), 5), ((600, 7, 9), 13), ((520, 6, 5), 20), ((514, 3, 2, 4), 9),
+                                       ((300, 4, 6), 24)])
+def test_mttkrp_large_mode1_paths(api, dims, rank):
+    from oracle import cp_oracle as O
+
+    rng = np.random.default_rng(sum(dims) + rank)
+    fac = [rng.standard_normal((d, rank)) for d in dims]
+    y = np.asfortranarray(rng.standard_normal(dims))
+    model = api.KruskalModel(fac)
+    for n in range(1, len(dims) + 1):
+        got = api.mttkrp(api.DenseTensor(y), model, n)
+        ref = O.mttkrp(y, fac, n)
+        assert _rel(got, ref) < 1e-13, f"mode {n}"
+    assert abs(api.relative_error(api.DenseTensor(y), model) - O.relative_error(y, fac)) < 1e-12
+
+
+def test_fit_large_mode1_matches_oracle(api):
+    from oracle import cp_oracle as O
+    from paper_1205_2584_b200 import synth
+
+    cfg = synth.scaled(synth.CONFIGS["c4"], (300, 12, 16), rank=6, max_iters=15, name="c4_wide")
+    y = synth.make_tensor(cfg, 0)
+    tau = synth.tau_for_unit_mu(cfg, 0)
+    res = api.fit(y, api.FitConfig(rank=6, tau=tau, tol=0.0, max_iters=15, seed=0, init="random"))
+    ref = O.fit_lm(y, O.OracleConfig(rank=6, tau=tau, tol=0.0, max_iters=15, seed=0))
+    assert "".join("A" if r.accepted else "r" for r in res.trace) == ref.accepted
+    assert abs(res.final_relerr - ref.final_relerr) < FIT_ATOL
+    assert _rel(res.model.as_vector(), O.stack(ref.factors)) < FACTOR_RTOL
