@@ -349,8 +349,8 @@ struct Engine final : EngineBase {
 
   template <int NT>
   void set_dmma_attrs() {
-    CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_dmma<NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)da_smem));
-    CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_dmma<NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)db_smem));
+    CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_dmma<NT, 0, kDmmaCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)da_smem));
+    CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_dmma<NT, 1, kDmmaCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)db_smem));
   }
   template <class F>
   void dispatch_nt(F&& f) {
@@ -379,13 +379,13 @@ struct Engine final : EngineBase {
       auto fill = [&](DmmaGeom& g) {
         g.I1 = I1; g.Lmid = Lmid; g.C = Cloc; g.WS = ws;
         g.tiles = (int)((I1 + kDmmaRows - 1) / kDmmaRows);
-        g.CK = 8;
+        g.CK = kDmmaCK;
         g.stage_elems = ((size_t)g.CK * (kDmmaSLp + ws) + 15) / 16 * 16;
       };
       fill(da);
       fill(db);
       const size_t sb = da.stage_elems * sizeof(double);
-      const size_t m1b = (size_t)8 * 8 * dm_nt * 2 * 32 * sizeof(double);
+      const size_t m1b = 0;  // M_1 accumulates in global (L2-resident) memory
       const size_t redb = (size_t)8 * 8 * dm_nt * sizeof(double);
       const size_t budget = (size_t)220 * 1024 - 128;
       if (m1b + redb + 2 * sb > budget) return;
@@ -585,7 +585,7 @@ struct Engine final : EngineBase {
                da.WS, (T*)WNd, cst, cfl, gate, 1);
         dispatch_nt([&](auto ntc) {
           constexpr int NTc = decltype(ntc)::value;
-          launch(k_pass_dmma<NTc, 0>, dim3(da.tiles, da_groups), dim3(kConsumers + 32), da_smem, (const double*)Y, da,
+          launch(k_pass_dmma<NTc, 0, kDmmaCK>, dim3(da.tiles, da_groups), dim3(kConsumers + 32), da_smem, (const double*)Y, da,
                  (const double*)WNd, (const double*)A1c, (const double*)KMc, RP, R, (double*)zpart, (double*)m1part,
                  cst, cfl, gate);
         });
@@ -661,7 +661,7 @@ struct Engine final : EngineBase {
           launch(k_krmid<T>, nblocks(Lmid * db.WS, 256), 256, 0, F, mg, Lmid, R, db.WS, (T*)KMd, cst, cfl, gate, 1);
         dispatch_nt([&](auto ntc) {
           constexpr int NTc = decltype(ntc)::value;
-          launch(k_pass_dmma<NTc, 1>, dim3(db.tiles, (unsigned)Cloc, db_chunks), dim3(kConsumers + 32), db_smem,
+          launch(k_pass_dmma<NTc, 1, kDmmaCK>, dim3(db.tiles, (unsigned)Cloc, db_chunks), dim3(kConsumers + 32), db_smem,
                  (const double*)Y, db, (const double*)KMd, (const double*)A1c, (const double*)KMc, RP, R, (double*)zpart,
                  (double*)bpart, cst, cfl, gate);
         });

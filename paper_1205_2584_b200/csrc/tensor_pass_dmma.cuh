@@ -21,6 +21,7 @@ namespace cpf {
 
 constexpr int kDmmaRows = 512;   // rows (i1) per CTA tile
 constexpr int kDmmaSLp = 516;    // padded smem row stride (== 4 mod 16 doubles)
+constexpr int kDmmaCK = 16;      // K rows per pipeline stage
 
 struct DmmaGeom {
   int64_t I1, Lmid, C;
@@ -38,7 +39,7 @@ __device__ __forceinline__ void dmma8x8x4(double& c0, double& c1, double a, doub
                : "d"(a), "d"(b));
 }
 
-template <int NT, int MODE>
+template <int NT, int MODE, int CKT>
 __global__ void __launch_bounds__(kConsumers + 32, 1) k_pass_dmma(const double* __restrict__ Y, DmmaGeom g,
                                                                   const double* __restrict__ Op,   // K rows x WS
                                                                   const double* __restrict__ A1c,  // I1 x RPg
@@ -51,8 +52,7 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) k_pass_dmma(const double* 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   double* stages = reinterpret_cast<double*>(smem_raw + 128);
-  double* m1s = stages + (size_t)g.NST * g.stage_elems;      // MODE 0: [8 warps][8][NT][2][32]
-  double* red = m1s + (MODE == 0 ? (size_t)8 * 8 * NT * 2 * 32 : 0);  // [8 warps][NCOL]
+  double* red = stages + (size_t)g.NST * g.stage_elems;  // [8 warps][NCOL]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int64_t tile = blockIdx.x;
@@ -77,16 +77,16 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) k_pass_dmma(const double* 
     kend = mend;
     nrb = 1;
   }
-  const int64_t nkc = (kend - kbeg + g.CK - 1) / g.CK;  // chunks per row block
+  const int64_t nkc = (kend - kbeg + CKT - 1) / CKT;  // chunks per row block
   const int64_t nq = nrb * nkc;
-  const size_t oofs = (size_t)g.CK * kDmmaSLp;
+  const size_t oofs = (size_t)CKT * kDmmaSLp;
   const uint32_t ybytes = (uint32_t)(rows_valid * sizeof(double));
 
   auto issue = [&](int64_t q) {
     const int s = (int)(q % g.NST);
     const int64_t rb = q / nkc, kc = q % nkc;
-    const int64_t k0 = kbeg + kc * g.CK;
-    const int ck = (int)min((int64_t)g.CK, kend - k0);
+    const int64_t k0 = kbeg + kc * CKT;
+    const int ck = (int)min((int64_t)CKT, kend - k0);
     double* dst = stages + (size_t)s * g.stage_elems;
     const uint32_t obytes = (uint32_t)(ck * g.WS * sizeof(double));
     fence_proxy_async();
@@ -124,34 +124,55 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) k_pass_dmma(const double* 
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  if (MODE == 0) {
-    for (int e = lane; e < 8 * NT * 2 * 32; e += 32) m1s[(size_t)wid * 8 * NT * 2 * 32 + e] = 0.0;
-  }
   const int rbase = wid * 64;
+  // MODE 0: the CTA's M_1 partial accumulates in place in m1_part (global, L2-resident: 96 KB per
+  // CTA, read-modify-written once per row block = once per C/4 k-steps)
+  double* m1g = m1_part + (int64_t)blockIdx.y * g.I1 * RPg;
+  if (MODE == 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t row = rbase + 8 * i + gq;
+      if (row >= rows_valid) continue;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = 8 * j + 2 * tq + h;
+          if (col < R) m1g[(a0 + row) * RPg + col] = 0.0;
+        }
+    }
+  }
 
+  int64_t rb = 0, kc = 0;
+  int s = 0;
+  uint32_t ph = 0;
   for (int64_t q = 0; q < nq; ++q) {
-    const int s = (int)(q % g.NST);
-    const int64_t rb = q / nkc, kc = q % nkc;
-    const int64_t k0 = kbeg + kc * g.CK;
-    const int ck = (int)min((int64_t)g.CK, kend - k0);
-    mbar_wait(&bars[s], (uint32_t)((q / g.NST) & 1));
+    const int64_t k0 = kbeg + kc * CKT;
+    const int ck = (int)min((int64_t)CKT, kend - k0);
+    mbar_wait(&bars[s], ph);
     const double* ys = stages + (size_t)s * g.stage_elems;
     const double* os = ys + oofs;
-    for (int ks = 0; ks < ck; ks += 4) {
-      const int kk = ks + tq;
+    double af[2][8], bf[2][NT];
+    auto load_frag = [&](int step, int b) {
+      const int kk = 4 * step + tq;
       const bool kv = kk < ck;
-      double af[8], bf[NT];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) af[i] = kv ? ys[(size_t)kk * kDmmaSLp + rbase + 8 * i + gq] : 0.0;
+      for (int i = 0; i < 8; ++i) af[b][i] = kv ? ys[(size_t)kk * kDmmaSLp + rbase + 8 * i + gq] : 0.0;
 #pragma unroll
-      for (int j = 0; j < NT; ++j) bf[j] = kv ? os[(size_t)kk * g.WS + 8 * j + gq] : 0.0;
+      for (int j = 0; j < NT; ++j) bf[b][j] = kv ? os[(size_t)kk * g.WS + 8 * j + gq] : 0.0;
+    };
+    load_frag(0, 0);
+#pragma unroll
+    for (int step = 0; step < CKT / 4; ++step) {
+      if (step + 1 < CKT / 4) load_frag(step + 1, (step + 1) & 1);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < NT; ++j) dmma8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < NT; ++j) dmma8x8x4(acc[i][j][0], acc[i][j][1], af[step & 1][i], bf[step & 1][j]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&bars[g.NST + s]);
+    if (++s == g.NST) { s = 0; ph ^= 1u; }
 
     if (MODE == 0 && kc == nkc - 1) {
       // ---- row-block epilogue for m = mbeg + rb
@@ -167,7 +188,6 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) k_pass_dmma(const double* 
           const int col = 8 * j + 2 * tq + h;
           km[j][h] = col < R ? __ldg(KMc + m * RPg + col) : 0.0;
         }
-      double* mw = m1s + (size_t)wid * 8 * NT * 2 * 32;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int64_t row = rbase + 8 * i + gq;
@@ -178,9 +198,11 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) k_pass_dmma(const double* 
           for (int h = 0; h < 2; ++h) {
             const int col = 8 * j + 2 * tq + h;
             const double p = acc[i][j][h];
-            double* mp = mw + (((size_t)i * NT + j) * 2 + h) * 32 + lane;
-            *mp = fma(p, km[j][h], *mp);
-            if (rv && col < R) zt[j][h] = fma(p, __ldg(A1c + (a0 + row) * RPg + col), zt[j][h]);
+            if (rv && col < R) {
+              double* mp = m1g + (a0 + row) * RPg + col;
+              *mp = fma(p, km[j][h], *mp);
+              zt[j][h] = fma(p, __ldg(A1c + (a0 + row) * RPg + col), zt[j][h]);
+            }
             acc[i][j][h] = 0.0;
           }
       }
@@ -203,25 +225,10 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) k_pass_dmma(const double* 
       }
       named_sync(1, kConsumers);
     }
+    if (++kc == nkc) { kc = 0; ++rb; }
   }
 
-  if (MODE == 0) {
-    // M_1 partial of this CTA: every (row, col) is owned by exactly one thread
-    const double* mw = m1s + (size_t)wid * 8 * NT * 2 * 32;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int64_t row = rbase + 8 * i + gq;
-      if (row >= rows_valid) continue;
-#pragma unroll
-      for (int j = 0; j < NT; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = 8 * j + 2 * tq + h;
-          if (col < R)
-            m1_part[((int64_t)blockIdx.y * g.I1 + a0 + row) * RPg + col] = mw[(((size_t)i * NT + j) * 2 + h) * 32 + lane];
-        }
-    }
-  } else {
+  if (MODE == 1) {
     // M_N partial: sum_i1 U[i1, col] conj(A_1[i1, col]) over the CTA's rows
     double zt[NT][2];
 #pragma unroll
