@@ -137,6 +137,12 @@ struct Engine final : EngineBase {
   T* invL = nullptr;
   size_t lu_smem = 0;
 
+  // CUDA graph of one iteration (replayed; all control is device-side)
+  cudaGraphExec_t gexec = nullptr;
+  int64_t graph_nodes = 0;
+  bool graph_ok = true;
+  static constexpr int kPoll = 4;  // iterations launched between host polls of the state
+
   // profiling
   bool prof = false;
   struct Ev { int ph; cudaEvent_t a, b; };
@@ -196,6 +202,7 @@ struct Engine final : EngineBase {
   ~Engine() override {
     cudaSetDevice(dev);
     if (s) cudaStreamSynchronize(s);
+    if (gexec) cudaGraphExecDestroy(gexec);
     for (auto& e : evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     void* ptrs[] = {Yown, A, Ac, M, Mc, D, G, Cand, V1, V2, V3, V4, Cg, Ccg, Gx, Gp, Gf, Gti, Gi, W1, Sm,
                     wvec, fvec, xvec, Phi, A1c, KMc, WNc, A1r, KMr, WNr, zpart, m1part, bpart, pa_out, pb_out, pb_all,
@@ -237,7 +244,7 @@ struct Engine final : EngineBase {
     dscal = dalloc<double>(16);
     red = dalloc<double>(4096);
     const int nblk32 = (nB + 31) / 32;
-    ibuf = dalloc<int>((size_t)2 * nB + 4 * kLuMaxKB + 8 + nblk32);
+    ibuf = dalloc<int>((size_t)2 * nB + 4 * kLuMaxKB + 8 + 2 * nblk32);
     lu.perm = ibuf;
     lu.ipiv = ibuf + nB;
     lu.gather = ibuf + 2 * nB;
@@ -843,12 +850,12 @@ struct Engine final : EngineBase {
     launch(k_perm_gather<T>, nblocks(nB, 256), 256, 0, w, (const int*)lu.perm, nB, xvec, (const LmDeviceState*)st,
            gate_running);
     const int nblk = (nB + 31) / 32;
-    ++epoch;
+    // ready flags are cleared in-stream (graph-replay safe: no host-side epoch)
     CPF_CUDA_CHECK(cudaMemsetAsync(lu.ticket, 0, sizeof(int) * 2, s));
-    launch(k_trsv<T, true>, nblk, 128, 0, (const T*)Phi, nB, nB, xvec, lu.ticket, lu.ready, epoch,
+    CPF_CUDA_CHECK(cudaMemsetAsync(lu.ready, 0, sizeof(int) * 2 * nblk, s));
+    launch(k_trsv<T, true>, nblk, 128, 0, (const T*)Phi, nB, nB, xvec, lu.ticket, lu.ready, 1,
            (const LmDeviceState*)st, gate_running);
-    ++epoch;
-    launch(k_trsv<T, false>, nblk, 128, 0, (const T*)Phi, nB, nB, xvec, lu.ticket + 1, lu.ready, epoch,
+    launch(k_trsv<T, false>, nblk, 128, 0, (const T*)Phi, nB, nB, xvec, lu.ticket + 1, lu.ready + nblk, 1,
            (const LmDeviceState*)st, gate_running);
     launch(k_apply_k<T>, nblocks(nB, 256), 256, 0, (const T*)xvec, N, R, (const T*)Gp, f, (const LmDeviceState*)st,
            gate_running);
@@ -974,6 +981,7 @@ struct Engine final : EngineBase {
   void set_tensor(const void* p, int64_t n, int where) override {
     if (n != Jloc) throw ApiError(CPF_E_ARG, "tensor slab size mismatch: expected " + std::to_string(Jloc));
     CPF_CUDA_CHECK(cudaSetDevice(dev));
+    if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }  // Y pointer is baked into the graph
     if (where == 1) {
       if (Yown) { CPF_CUDA_CHECK(cudaFree(Yown)); Yown = nullptr; }
       Y = static_cast<const T*>(p);
@@ -1091,10 +1099,41 @@ struct Engine final : EngineBase {
     launch(k_clear_pending, 1, 1, 0, fl);
   }
 
+  void capture_iteration() {
+    cudaGraph_t g = nullptr;
+    const int64_t before = nlaunch;
+    CPF_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+      iteration();
+    } catch (...) {
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    CPF_CUDA_CHECK(cudaStreamEndCapture(s, &g));
+    CPF_CUDA_CHECK(cudaGraphInstantiate(&gexec, g, 0));
+    cudaGraphDestroy(g);
+    graph_nodes = nlaunch - before;
+    nlaunch = before;
+  }
+
   void fit_step(int n, cpf_status* o) override {
     pull_state();
-    for (int k = 0; k < n && hst->stopped == 0; ++k) {
-      iteration();
+    const char* env = getenv("CPF_NO_GRAPH");
+    const bool use_graph = graph_ok && !prof && !(env && env[0] == '1');
+    if (use_graph && !gexec) capture_iteration();
+    int k = 0;
+    while (k < n && hst->stopped == 0) {
+      const int batch = use_graph ? std::min(kPoll, n - k) : 1;
+      for (int b = 0; b < batch; ++b) {
+        if (use_graph) {
+          CPF_CUDA_CHECK(cudaGraphLaunch(gexec, s));
+          nlaunch += graph_nodes;
+        } else {
+          iteration();
+        }
+      }
+      k += batch;
       pull_state();
     }
     fill_status(o);
