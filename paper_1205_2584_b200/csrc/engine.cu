@@ -313,34 +313,31 @@ struct Engine final : EngineBase {
                                         (int)(2 * R * R * sizeof(T))));
   }
 
+  int lu3_thr = 128;  // threads per CTA of the register panel
   void plan_lu3() {
     invL = dalloc<T>(kLuMaxKB * kLuMaxKB);
     lu3_rpt = 0;
-    const int maxrpt = sizeof(T) == 16 ? 1 : 3;
-    for (int r = 1; r <= maxrpt; ++r)
-      if ((nB + 256 * r - 1) / (256 * r) <= 8) { lu3_rpt = r; break; }
-    if (!lu3_rpt && (nB + 256 * maxrpt - 1) / (256 * maxrpt) <= 16) lu3_rpt = maxrpt;
+    // (rows/thread, threads/CTA) candidates, smallest per-SM work first; cluster <= 16 CTAs
+    const int cand[2][2] = {{1, 128}, {sizeof(T) == 8 ? 2 : 1, 256}};
+    for (auto& c : cand)
+      if ((nB + c[0] * c[1] - 1) / (c[0] * c[1]) <= 16) { lu3_rpt = c[0]; lu3_thr = c[1]; break; }
     if (!lu3_rpt) return;  // fall back to the smem panel
-    const size_t smem = panel3_smem_bytes<T>(16, kLuMaxKB);
-    auto setattr = [&](auto kern) {
+    auto setattr = [&](auto kern, int thr) {
+      const size_t smem = panel3_smem_bytes<T>(16, kLuMaxKB, thr);
       CPF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       CPF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     };
-    if constexpr (sizeof(T) == 8) {
-      setattr(k_panel_lu3<T, kLuMaxKB, 1>);
-      setattr(k_panel_lu3<T, kLuMaxKB, 2>);
-      setattr(k_panel_lu3<T, kLuMaxKB, 3>);
-    } else {
-      setattr(k_panel_lu3<T, kLuMaxKB, 1>);
-    }
+    setattr(k_panel_lu3<T, kLuMaxKB, 1, 128>, 128);
+    if constexpr (sizeof(T) == 8) setattr(k_panel_lu3<T, kLuMaxKB, 2, 256>, 256);
+    else setattr(k_panel_lu3<T, kLuMaxKB, 1, 256>, 256);
   }
 
-  template <int RPTc>
+  template <int RPTc, int THR>
   void launch_panel3(int k0, int kb, int cl, int gate_running) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cl);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = panel3_smem_bytes<T>(cl, kLuMaxKB);
+    cfg.blockDim = dim3(THR);
+    cfg.dynamicSmemBytes = panel3_smem_bytes<T>(cl, kLuMaxKB, THR);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -349,7 +346,7 @@ struct Engine final : EngineBase {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_panel_lu3<T, kLuMaxKB, RPTc>, Phi, nB, nB, k0, kb, lu, invL,
+    CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_panel_lu3<T, kLuMaxKB, RPTc, THR>, Phi, nB, nB, k0, kb, lu, invL,
                                       (const LmDeviceState*)st, gate_running));
     ++nlaunch;
   }
@@ -793,12 +790,10 @@ struct Engine final : EngineBase {
       const int kb = std::min(kbmax, nB - k0);
       const int m = nB - k0;
       if (lu3_rpt) {
-        const int cl = (m + 256 * lu3_rpt - 1) / (256 * lu3_rpt);
-        if (lu3_rpt == 1) launch_panel3<1>(k0, kb, cl, gate_running);
-        else if constexpr (sizeof(T) == 8) {
-          if (lu3_rpt == 2) launch_panel3<2>(k0, kb, cl, gate_running);
-          else launch_panel3<3>(k0, kb, cl, gate_running);
-        }
+        const int cl = (m + lu3_thr * lu3_rpt - 1) / (lu3_thr * lu3_rpt);
+        if (lu3_thr == 128) launch_panel3<1, 128>(k0, kb, cl, gate_running);
+        else if constexpr (sizeof(T) == 8) launch_panel3<2, 256>(k0, kb, cl, gate_running);
+        else launch_panel3<1, 256>(k0, kb, cl, gate_running);
       } else {
         int cl = lu_cl;
         const int rpc = (m + cl - 1) / cl;

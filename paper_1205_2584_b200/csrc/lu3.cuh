@@ -26,26 +26,27 @@ __device__ __forceinline__ cplx shfl_val<cplx>(cplx v, int src) {
 }
 
 template <class T>
-size_t panel3_smem_bytes(int CL, int KB) {
-  const size_t NC = (size_t)CL * 8;
-  size_t b = sizeof(T) * (2 * NC * KB + (size_t)KB * KB);
+size_t panel3_smem_bytes(int CL, int KB, int nthr) {
+  const size_t NC = (size_t)CL * (nthr / 32);
+  size_t b = sizeof(T) * (2 * NC * KB + (size_t)KB * KB + (size_t)(nthr / 32) * KB);
   b += sizeof(double) * 2 * NC + sizeof(int) * 2 * NC + sizeof(int) * 4 * KB;
   return (b + 15) & ~(size_t)15;
 }
 
-template <class T, int KB, int RPT>
-__global__ void __launch_bounds__(256, 1) k_panel_lu3(T* __restrict__ A, int n, int lda, int k0, int kb, LuWork w,
-                                                      T* __restrict__ invL, const LmDeviceState* st, int gate_running) {
+template <class T, int KB, int RPT, int NTHR>
+__global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n, int lda, int k0, int kb, LuWork w,
+                                                       T* __restrict__ invL, const LmDeviceState* st, int gate_running) {
   if (st && gate_running && (st->stopped || st->err_code)) return;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
-  constexpr int NW = 8;
+  constexpr int NW = NTHR / 32;
   const int NC = CL * NW;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* cand_data = reinterpret_cast<T*>(smem_raw);            // [2][NC][KB]
   T* top = cand_data + (size_t)2 * NC * KB;                  // [KB][KB] row jj = pivot row jj
-  double* cand_val = reinterpret_cast<double*>(top + (size_t)KB * KB);
+  T* wrow_s = top + (size_t)KB * KB;                         // [NW][KB] staging of each warp's candidate
+  double* cand_val = reinterpret_cast<double*>(wrow_s + (size_t)NW * KB);
   int* cand_row = reinterpret_cast<int*>(cand_val + 2 * NC);
   int* pivrows = cand_row + 2 * NC;                          // [KB]
   int* Dl = pivrows + KB;                                    // [KB]
@@ -54,33 +55,26 @@ __global__ void __launch_bounds__(256, 1) k_panel_lu3(T* __restrict__ A, int n, 
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int m = n - k0;
-  const int cta_rows = 256 * RPT;
+  const int cta_rows = NTHR * RPT;
   T a[RPT][KB];
   bool alive[RPT];
   int myrow[RPT];  // panel-relative row index
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    myrow[j] = rank * cta_rows + j * 256 + tid;
+    myrow[j] = rank * cta_rows + j * NTHR + tid;
     alive[j] = myrow[j] < m;
     const T* src = A + (int64_t)(k0 + myrow[j]) + (int64_t)lda * k0;
 #pragma unroll
     for (int q = 0; q < KB; ++q) a[j][q] = (alive[j] && q < kb) ? src[(int64_t)lda * q] : zero_of<T>();
   }
+  T cur[RPT];  // a[j][jj] of the current column, maintained by the elimination loop
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) cur[j] = a[j][0];
 
-  // The column loop is NOT unrolled (a fully unrolled 32-column body is ~30K SASS instructions
-  // and thrashes the instruction cache); register rows are addressed with static indices by
-  // selecting / predicating over q.
+  // Column loop NOT unrolled (I-cache); registers addressed statically by predication over q.
 #pragma unroll 1
   for (int jj = 0; jj < kb; ++jj) {
     const int par = jj & 1;
-    T cur[RPT];
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-      cur[j] = a[j][0];
-#pragma unroll
-      for (int q = 1; q < KB; ++q)
-        if (q == jj) cur[j] = a[j][q];
-    }
     // ---- my best alive row, then warp argmax (ties -> smaller row)
     double bv = -1.0;
     int bj = 0, brow = 0x7fffffff;
@@ -99,17 +93,20 @@ __global__ void __launch_bounds__(256, 1) k_panel_lu3(T* __restrict__ A, int n, 
       const int ol = __shfl_xor_sync(0xffffffffu, wlane, o);
       if (ov > wv || (ov == wv && orow < wrow)) { wv = ov; wrow = orow; wlane = ol; }
     }
-    // ---- broadcast the warp's candidate row: lane q receives element q
-    T mine = zero_of<T>();
+    // ---- the warp's best lane stages its row in shared memory; lane q then owns element q
+    if (lane == wlane) {
+      T* dst = wrow_s + wid * KB;
 #pragma unroll
-    for (int q = 0; q < KB; ++q) {
-      T sel = a[0][q];
+      for (int q = 0; q < KB; ++q) {
+        T sel = a[0][q];
 #pragma unroll
-      for (int j = 1; j < RPT; ++j)
-        if (bj == j) sel = a[j][q];
-      const T got = shfl_val(sel, wlane);
-      if (lane == q) mine = got;
+        for (int j = 1; j < RPT; ++j)
+          if (bj == j) sel = a[j][q];
+        dst[q] = sel;
+      }
     }
+    __syncwarp();
+    const T mine = wrow_s[wid * KB + lane];
     const int slot = par * NC + rank * NW + wid;
     for (int r = 0; r < CL; ++r) {
       if (lane < kb) cluster.map_shared_rank(cand_data, r)[(size_t)slot * KB + lane] = mine;
@@ -143,14 +140,16 @@ __global__ void __launch_bounds__(256, 1) k_panel_lu3(T* __restrict__ A, int n, 
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
       if (alive[j] && myrow[j] == cr) alive[j] = false;
-      if (alive[j] && !zero_piv) {
-        const T l = dvd(cur[j], piv);
+      const bool el = alive[j] && !zero_piv;
+      const T l = el ? dvd(cur[j], piv) : zero_of<T>();
+      T nx = zero_of<T>();
 #pragma unroll
-        for (int q = 0; q < KB; ++q) {
-          if (q == jj) a[j][q] = l;
-          else if (q > jj) fms_acc(a[j][q], l, prow[q]);
-        }
+      for (int q = 0; q < KB; ++q) {
+        if (q > jj) fms_acc(a[j][q], l, prow[q]);
+        if (q == jj && el) a[j][q] = l;
+        if (q == jj + 1) nx = a[j][q];
       }
+      cur[j] = nx;
     }
   }
   __syncthreads();
@@ -185,7 +184,7 @@ __global__ void __launch_bounds__(256, 1) k_panel_lu3(T* __restrict__ A, int n, 
   }
   if (rank == 0) {
     // pivot rows -> top block positions
-    for (int e = tid; e < kb * kb; e += 256) {
+    for (int e = tid; e < kb * kb; e += NTHR) {
       const int r = e % kb, q = e / kb;
       A[(int64_t)(k0 + r) + (int64_t)lda * (k0 + q)] = top[r * KB + q];
     }
