@@ -335,6 +335,17 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// spin with relaxed loads (no L1 invalidation per poll), then one acquire load
+__device__ __forceinline__ void wait_flag(const int* p, int v) {
+  while (ld_relaxed_gpu(p) != v) {
+  }
+  (void)ld_acquire_gpu(p);
+}
 __device__ __forceinline__ void st_release_gpu(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -369,6 +380,13 @@ __global__ void __launch_bounds__(128) k_trsv(const T* __restrict__ A, int n, in
   const int rows = min(32, n - r0);
   const int row = r0 + lane;
   const bool rv = row < n;
+  // prefetch (off the critical path): the diagonal tile and this block's right-hand side
+  T dg[32];
+  T v0 = zero_of<T>();
+  if (wid == 0) {
+    load_tile_col(A, lda, row, rv, r0, rows, dg);
+    v0 = rv ? ld_cg(x + row) : zero_of<T>();
+  }
   T acc = zero_of<T>();
   {
     T cur[32], nxt[32];
@@ -386,10 +404,7 @@ __global__ void __launch_bounds__(128) k_trsv(const T* __restrict__ A, int n, in
         const int kbn = LOWER ? qn : (nblk - 1 - qn);
         load_tile_col(A, lda, row, rv, kbn * 32, min(32, n - kbn * 32), nxt);
       }
-      if (lane == 0) {
-        while (ld_acquire_gpu(ready + kblk) != epoch) {
-        }
-      }
+      if (lane == 0) wait_flag(ready + kblk, epoch);
       __syncwarp();
       const T xv = (lane < cols) ? ld_cg(x + c0 + lane) : zero_of<T>();
 #pragma unroll
@@ -402,10 +417,7 @@ __global__ void __launch_bounds__(128) k_trsv(const T* __restrict__ A, int n, in
   part[wid][lane] = acc;
   __syncthreads();
   if (wid == 0) {
-    T dg[32];
-    load_tile_col(A, lda, row, rv, r0, rows, dg);
-    T v = rv ? ld_cg(x + row) : zero_of<T>();
-    v = add(v, add(add(part[0][lane], part[1][lane]), add(part[2][lane], part[3][lane])));
+    T v = add(v0, add(add(part[0][lane], part[1][lane]), add(part[2][lane], part[3][lane])));
     if (LOWER) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
