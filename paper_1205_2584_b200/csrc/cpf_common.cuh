@@ -60,6 +60,12 @@ __host__ __device__ __forceinline__ cplx dvd(cplx a, cplx b) {
     return cplx{(a.x * r + a.y) / d, (a.y * r - a.x) / d};
   }
 }
+// 1/a via the hardware-seeded IEEE reciprocal (__drcp_rn): avoids the long div.rn.f64 sequence
+__device__ __forceinline__ double rcp_of(double a) { return __drcp_rn(a); }
+__device__ __forceinline__ cplx rcp_of(cplx a) {
+  const double s = __drcp_rn(a.x * a.x + a.y * a.y);
+  return cplx{a.x * s, -a.y * s};
+}
 // modulus |a| (np.abs): hypot for complex
 __host__ __device__ __forceinline__ double modulus(double a) { return fabs(a); }
 __host__ __device__ __forceinline__ double modulus(cplx a) { return hypot(a.x, a.y); }
@@ -231,4 +237,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // named barrier over the first `nthreads` threads (consumer warps only)
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// DSMEM: address of `p` (this CTA's shared memory) in CTA `rank` of the cluster, and stores to it
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, cplx v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }

@@ -319,8 +319,12 @@ struct Engine final : EngineBase {
     lu3_rpt = 0;
     // (rows/thread, threads/CTA) candidates, smallest per-SM work first; cluster <= 16 CTAs
     const int cand[2][2] = {{1, 128}, {sizeof(T) == 8 ? 2 : 1, 256}};
-    for (auto& c : cand)
+    int start = 0;
+    if (const char* e = getenv("CPF_PANEL_WIDE")) if (e[0] == '1') start = 1;  // experiment knob
+    for (int ci = start; ci < 2; ++ci) {
+      const auto& c = cand[ci];
       if ((nB + c[0] * c[1] - 1) / (c[0] * c[1]) <= 16) { lu3_rpt = c[0]; lu3_thr = c[1]; break; }
+    }
     if (!lu3_rpt) return;  // fall back to the smem panel
     auto setattr = [&](auto kern, int thr) {
       const size_t smem = panel3_smem_bytes<T>(16, kLuMaxKB, thr);
@@ -1356,3 +1360,7 @@ int cpf_engine_phase_times(cpf_engine* e, double* ms_out, int64_t* counts_out, i
 int64_t cpf_engine_launch_count(const cpf_engine* e) { return (e && e->impl) ? e->impl->launches() : 0; }
 
 }  // extern "C"
+
+extern "C" int cpf_debug_panel_cycles(long long* out8) {
+  return cudaMemcpyFromSymbol(out8, cpf::g_panel_cycles, sizeof(long long) * 8) == cudaSuccess ? 0 : -4;
+}

@@ -16,6 +16,9 @@
 
 namespace cpf {
 
+// per-phase cycle counters of the panel kernel (CTA 0, thread 0), enabled with -DCPF_PANEL_TIMING
+__device__ long long g_panel_cycles[8];
+
 template <class T>
 __device__ __forceinline__ T shfl_val(T v, int src);
 template <>
@@ -27,10 +30,26 @@ __device__ __forceinline__ cplx shfl_val<cplx>(cplx v, int src) {
 
 template <class T>
 size_t panel3_smem_bytes(int CL, int KB, int nthr) {
-  const size_t NC = (size_t)CL * (nthr / 32);
-  size_t b = sizeof(T) * (2 * NC * KB + (size_t)KB * KB + (size_t)(nthr / 32) * KB);
+  const size_t NC = (size_t)CL;  // one candidate per CTA
+  const size_t NW = (size_t)nthr / 32;
+  size_t b = sizeof(T) * (2 * NC * KB + (size_t)KB * KB + NW * KB + 2 * NC);  // + rcp slots
   b += sizeof(double) * 2 * NC + sizeof(int) * 2 * NC + sizeof(int) * 4 * KB;
+  b += sizeof(double) * NW + sizeof(int) * NW;  // per-warp keys
   return (b + 15) & ~(size_t)15;
+}
+
+// Warp argmax of non-negative doubles with ties broken by the smaller row (redux-based: 3
+// warp reductions instead of a 5-round shuffle tree).  Returns the winning value/row/lane.
+__device__ __forceinline__ void warp_argmax_redux(double v, int row, double& wv, int& wrow, int& wlane) {
+  const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
+  const unsigned m1 = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned m2 = __reduce_max_sync(0xffffffffu, hi == m1 ? lo : 0u);
+  const bool cand = (hi == m1) && (lo == m2);
+  const unsigned r = (unsigned)__reduce_min_sync(0xffffffffu, cand ? (unsigned)row : 0x7fffffffu);
+  const unsigned bal = __ballot_sync(0xffffffffu, cand && (unsigned)row == r);
+  wlane = __ffs(bal) - 1;
+  wrow = (int)r;
+  wv = __hiloint2double((int)m1, (int)m2);
 }
 
 template <class T, int KB, int RPT, int NTHR>
@@ -41,12 +60,16 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
   const int CL = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
   constexpr int NW = NTHR / 32;
-  const int NC = CL * NW;
+  const int NC = CL;  // one published candidate per CTA
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* cand_data = reinterpret_cast<T*>(smem_raw);            // [2][NC][KB]
   T* top = cand_data + (size_t)2 * NC * KB;                  // [KB][KB] row jj = pivot row jj
   T* wrow_s = top + (size_t)KB * KB;                         // [NW][KB] staging of each warp's candidate
-  double* cand_val = reinterpret_cast<double*>(wrow_s + (size_t)NW * KB);
+  T* cand_rcp = wrow_s + (size_t)NW * KB;                    // [2][NC] 1/pivot of each candidate
+  T* wrcp = cand_rcp + 2 * NC;                               // [NW] 1/pivot of each warp candidate
+  double* wkey_v = reinterpret_cast<double*>(wrcp + NW);     // [NW]
+  int* wkey_r = reinterpret_cast<int*>(wkey_v + NW);               // [NW]
+  double* cand_val = reinterpret_cast<double*>(wkey_r + NW);
   int* cand_row = reinterpret_cast<int*>(cand_val + 2 * NC);
   int* pivrows = cand_row + 2 * NC;                          // [KB]
   int* Dl = pivrows + KB;                                    // [KB]
@@ -67,33 +90,45 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
 #pragma unroll
     for (int q = 0; q < KB; ++q) a[j][q] = (alive[j] && q < kb) ? src[(int64_t)lda * q] : zero_of<T>();
   }
+  // DSMEM bases of the candidate slots in every CTA of the cluster (same layout everywhere)
+  uint32_t rbase_data[16], rbase_val[16], rbase_row[16], rbase_rcp[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r)
+    if (r < CL) {
+      rbase_data[r] = mapa_u32(cand_data, r);
+      rbase_val[r] = mapa_u32(cand_val, r);
+      rbase_row[r] = mapa_u32(cand_row, r);
+      rbase_rcp[r] = mapa_u32(cand_rcp, r);
+    }
   T cur[RPT];  // a[j][jj] of the current column, maintained by the elimination loop
 #pragma unroll
   for (int j = 0; j < RPT; ++j) cur[j] = a[j][0];
 
   // Column loop NOT unrolled (I-cache); registers addressed statically by predication over q.
+#ifdef CPF_PANEL_TIMING
+  long long tacc[6] = {0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+#define PT(i) do { long long tn = clock64(); tacc[i] += tn - tprev; tprev = tn; } while (0)
+#else
+#define PT(i) do {} while (0)
+#endif
 #pragma unroll 1
   for (int jj = 0; jj < kb; ++jj) {
     const int par = jj & 1;
-    // ---- my best alive row, then warp argmax (ties -> smaller row)
-    double bv = -1.0;
+    // ---- (a) my best alive row, then warp argmax (ties -> smaller row)
+    double bv = 0.0;
     int bj = 0, brow = 0x7fffffff;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
-      const double v = alive[j] ? pivmag(cur[j]) : -1.0;
-      if (v > bv) { bv = v; bj = j; brow = myrow[j]; }
+      if (!alive[j]) continue;
+      const double v = pivmag(cur[j]);
+      if (brow == 0x7fffffff || v > bv) { bv = v; bj = j; brow = myrow[j]; }
     }
-    double wv = bv;
-    int wrow = (bv >= 0.0) ? brow : 0x7fffffff;
-    int wlane = lane;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, wv, o);
-      const int orow = __shfl_xor_sync(0xffffffffu, wrow, o);
-      const int ol = __shfl_xor_sync(0xffffffffu, wlane, o);
-      if (ov > wv || (ov == wv && orow < wrow)) { wv = ov; wrow = orow; wlane = ol; }
-    }
-    // ---- the warp's best lane stages its row in shared memory; lane q then owns element q
+    double wv;
+    int wrow, wlane;
+    warp_argmax_redux(bv, brow, wv, wrow, wlane);
+    PT(0);
+    // ---- (b) the warp's best lane stages its row; lane 0 posts the warp key
     if (lane == wlane) {
       T* dst = wrow_s + wid * KB;
 #pragma unroll
@@ -104,54 +139,79 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
           if (bj == j) sel = a[j][q];
         dst[q] = sel;
       }
+      wkey_v[wid] = wv;
+      wkey_r[wid] = wrow;
     }
-    __syncwarp();
-    const T mine = wrow_s[wid * KB + lane];
-    const int slot = par * NC + rank * NW + wid;
-    for (int r = 0; r < CL; ++r) {
-      if (lane < kb) cluster.map_shared_rank(cand_data, r)[(size_t)slot * KB + lane] = mine;
-      if (lane == 0) {
-        cluster.map_shared_rank(cand_val, r)[slot] = wv;
-        cluster.map_shared_rank(cand_row, r)[slot] = wrow;
+    __syncthreads();
+    // ---- (c) warp 0: CTA argmax over the NW warp keys, publish the CTA candidate cluster-wide
+    if (wid == 0) {
+      const double kv = lane < NW ? wkey_v[lane] : 0.0;
+      const int kr = lane < NW ? wkey_r[lane] : 0x7fffffff;
+      double cv;
+      int crow, cw;
+      warp_argmax_redux(kv, kr, cv, crow, cw);
+      const T mine = wrow_s[cw * KB + lane];
+      const T pj = wrow_s[cw * KB + jj];
+      const T rc = (lane == 0 && cv != 0.0) ? rcp_of(pj) : zero_of<T>();
+      const uint32_t doff = (uint32_t)(((size_t)(par * NC + rank) * KB + lane) * sizeof(T));
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        if (r < CL) {
+          if (lane < kb) st_cluster(rbase_data[r] + doff, mine);
+          if (lane == 0) {
+            st_cluster(rbase_val[r] + (uint32_t)((par * NC + rank) * sizeof(double)), cv);
+            st_cluster(rbase_row[r] + (uint32_t)((par * NC + rank) * sizeof(int)), crow);
+            st_cluster(rbase_rcp[r] + (uint32_t)((par * NC + rank) * sizeof(T)), rc);
+          }
+        }
       }
     }
+    PT(1);
     cluster.sync();
-    // ---- winner among the NC candidates (warp-parallel, identical everywhere)
-    double cv = -2.0;
-    int cr = 0x7fffffff, cs = 0;
-    for (int q = lane; q < NC; q += 32) {
-      const double v = cand_val[par * NC + q];
-      const int rr = cand_row[par * NC + q];
-      if (v > cv || (v == cv && rr < cr)) { cv = v; cr = rr; cs = q; }
+    PT(2);
+    // ---- (d) winner among the CL CTA candidates (identical everywhere)
+    double gv;
+    int grow, gl;
+    {
+      const double v = lane < NC ? cand_val[par * NC + lane] : 0.0;
+      const int rr = lane < NC ? cand_row[par * NC + lane] : 0x7fffffff;
+      warp_argmax_redux(v, rr, gv, grow, gl);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
-      const int orr = __shfl_xor_sync(0xffffffffu, cr, o);
-      const int os = __shfl_xor_sync(0xffffffffu, cs, o);
-      if (ov > cv || (ov == cv && orr < cr)) { cv = ov; cr = orr; cs = os; }
-    }
+    const int cs = gl;
+    const int cr = grow;
     const T* prow = cand_data + ((size_t)par * NC + cs) * KB;
-    const T piv = prow[jj];
-    const bool zero_piv = (pivmag(piv) == 0.0);
+    const T rcp = cand_rcp[par * NC + cs];
+    const bool zero_piv = (gv == 0.0);
     if (tid == 0) pivrows[jj] = k0 + cr;
     if (tid < KB) top[jj * KB + tid] = prow[tid];
     if (zero_piv && rank == 0 && tid == 0 && *w.info == 0) *w.info = k0 + jj + 1;
+    PT(3);
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
       if (alive[j] && myrow[j] == cr) alive[j] = false;
       const bool el = alive[j] && !zero_piv;
-      const T l = el ? dvd(cur[j], piv) : zero_of<T>();
+      const T l = el ? mul(cur[j], rcp) : zero_of<T>();
       T nx = zero_of<T>();
 #pragma unroll
-      for (int q = 0; q < KB; ++q) {
-        if (q > jj) fms_acc(a[j][q], l, prow[q]);
-        if (q == jj && el) a[j][q] = l;
-        if (q == jj + 1) nx = a[j][q];
+      for (int c8 = 0; c8 < KB; c8 += 8) {
+        if (c8 + 7 < jj) continue;  // uniform: chunk entirely left of the pivot column
+#pragma unroll
+        for (int q = c8; q < c8 + 8; ++q) {
+          if (q > jj) fms_acc(a[j][q], l, prow[q]);
+          if (q == jj && el) a[j][q] = l;
+          if (q == jj + 1) nx = a[j][q];
+        }
       }
       cur[j] = nx;
     }
+    PT(4);
   }
+#ifdef CPF_PANEL_TIMING
+  if (rank == 0 && tid == 0)
+    for (int i = 0; i < 5; ++i) atomicAdd((unsigned long long*)&g_panel_cycles[i], (unsigned long long)tacc[i]);
+  if (rank == 0 && tid == 0) atomicAdd((unsigned long long*)&g_panel_cycles[7], 1ull);
+#endif
+#undef PT
   __syncthreads();
   // ---- interchange bookkeeping (same rule as k_panel_lu): D (non-pivot top rows, ascending)
   // -> V (pivot rows from below, pick order)
