@@ -134,7 +134,10 @@ struct Engine final : EngineBase {
   int ga_groups = 1, gb_chunks = 1;
   int lu_kb = 32, lu_cl = 1, lu_rpc = 0;
   int lu3_rpt = 1;      // rows per thread of the register-resident panel (0: use the smem panel)
-  T* invL = nullptr;
+  T* invL = nullptr;    // 2 slots (double-buffered across look-ahead steps)
+  int* gring = nullptr; // 2 gather lists + counts
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t evP = nullptr, evB = nullptr, evJ = nullptr;
   size_t lu_smem = 0;
 
   // CUDA graph of one iteration (replayed; all control is device-side)
@@ -203,10 +206,14 @@ struct Engine final : EngineBase {
     cudaSetDevice(dev);
     if (s) cudaStreamSynchronize(s);
     if (gexec) cudaGraphExecDestroy(gexec);
+    if (evP) cudaEventDestroy(evP);
+    if (evB) cudaEventDestroy(evB);
+    if (evJ) cudaEventDestroy(evJ);
+    if (s2) cudaStreamDestroy(s2);
     for (auto& e : evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     void* ptrs[] = {Yown, A, Ac, M, Mc, D, G, Cand, V1, V2, V3, V4, Cg, Ccg, Gx, Gp, Gf, Gti, Gi, W1, Sm,
                     wvec, fvec, xvec, Phi, A1c, KMc, WNc, A1r, KMr, WNr, zpart, m1part, bpart, pa_out, pb_out, pb_all,
-                    norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL, WNd, KMd};
+                    norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL, WNd, KMd, gring};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (hst) cudaFreeHost(hst);
@@ -315,7 +322,12 @@ struct Engine final : EngineBase {
 
   int lu3_thr = 128;  // threads per CTA of the register panel
   void plan_lu3() {
-    invL = dalloc<T>(kLuMaxKB * kLuMaxKB);
+    invL = dalloc<T>(2 * kLuMaxKB * kLuMaxKB);
+    gring = dalloc<int>(2 * (4 * kLuMaxKB + 4));
+    CPF_CUDA_CHECK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evP, cudaEventDisableTiming));
+    CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
+    CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evJ, cudaEventDisableTiming));
     lu3_rpt = 0;
     // (rows/thread, threads/CTA) candidates, smallest per-SM work first; cluster <= 16 CTAs
     const int cand[2][2] = {{1, 128}, {sizeof(T) == 8 ? 2 : 1, 256}};
@@ -337,7 +349,7 @@ struct Engine final : EngineBase {
   }
 
   template <int RPTc, int THR>
-  void launch_panel3(int k0, int kb, int cl, int gate_running) {
+  void launch_panel3(int k0, int kb, int cl, int gate_running, LuWork wk, T* invl) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cl);
     cfg.blockDim = dim3(THR);
@@ -350,7 +362,7 @@ struct Engine final : EngineBase {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_panel_lu3<T, kLuMaxKB, RPTc, THR>, Phi, nB, nB, k0, kb, lu, invL,
+    CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_panel_lu3<T, kLuMaxKB, RPTc, THR>, Phi, nB, nB, k0, kb, wk, invl,
                                       (const LmDeviceState*)st, gate_running));
     ++nlaunch;
   }
@@ -786,19 +798,80 @@ struct Engine final : EngineBase {
   }
 
   // ---- LU of Phi and the B-application
+  // trailing update of panel (k0, kb) restricted to columns [c0, c1): U12 there, then A22 -= L21 U12
+  void lu_update_cols(int k0, int kb, int c0, int c1, const T* invl, cudaStream_t strm, int gr) {
+    if (c1 <= c0) return;
+    const int w = c1 - c0, rows = nB - k0 - kb;
+    k_u12<T, kLuMaxKB><<<nblocks(w, 64), 256, 0, strm>>>(Phi, c1, nB, k0, kb, invl, (const LmDeviceState*)st, gr, c0);
+    ++nlaunch;
+    CPF_CUDA_CHECK(cudaGetLastError());
+    if (rows <= 0) return;
+    if constexpr (sizeof(T) == 8)
+      k_gemm_dmma<<<dim3(nblocks(rows, 64), nblocks(w, 64)), 128, 0, strm>>>(Phi, nB, k0 + kb, c0, k0, rows, w, kb,
+                                                                            (const LmDeviceState*)st, gr);
+    else
+      k_gemm_sub<T><<<dim3(nblocks(rows, 64), nblocks(w, 64)), 256, 0, strm>>>(Phi, nB, k0 + kb, c0, k0, rows, w, kb,
+                                                                              (const LmDeviceState*)st, gr);
+    ++nlaunch;
+    CPF_CUDA_CHECK(cudaGetLastError());
+  }
+  void lu_gather(int slot, int ca0, int ca1, int cb0, int cb1, int do_perm, cudaStream_t strm, int gr) {
+    const int cols = std::max(0, ca1 - ca0) + std::max(0, cb1 - cb0);
+    const int cb = 256 / (2 * kLuMaxKB);
+    int* g = gring + slot * (4 * kLuMaxKB + 4);
+    k_row_gather2<T><<<std::max(1u, nblocks(cols, cb)), 256, 256 * sizeof(T), strm>>>(
+        Phi, nB, g, g + 4 * kLuMaxKB, lu.perm, ca0, ca1, cb0, cb1, do_perm, (const LmDeviceState*)st, gr);
+    ++nlaunch;
+    CPF_CUDA_CHECK(cudaGetLastError());
+  }
+
   void lu_factor(int gate_running) {
     ph_begin(kPhLU);
     launch(k_lu_init, nblocks(nB, 256), 256, 0, lu.perm, nB, lu.info);
-    const int kbmax = lu3_rpt ? kLuMaxKB : lu_kb;
+    if (lu3_rpt) {
+      // Look-ahead right-looking LU: stream s factors panel k and updates only the next block
+      // (the columns panel k+1 needs); stream s2 applies panel k to everything else concurrently
+      // with panel k+1.  Gather lists and inv(L11) are double-buffered across steps.
+      const int KB = kLuMaxKB;
+      const int np = (nB + KB - 1) / KB;
+      CPF_CUDA_CHECK(cudaEventRecord(evJ, s));
+      CPF_CUDA_CHECK(cudaStreamWaitEvent(s2, evJ, 0));
+      for (int k = 0; k < np; ++k) {
+        const int k0 = k * KB, kb = std::min(KB, nB - k0), m = nB - k0;
+        const int slot = k & 1;
+        LuWork wk = lu;
+        wk.gather = gring + slot * (4 * KB + 4);
+        wk.gcount = wk.gather + 4 * KB;
+        T* invl = invL + (size_t)slot * KB * KB;
+        // panel k only needs the next block of step k-1, already updated on s
+        const int cl = (m + lu3_thr * lu3_rpt - 1) / (lu3_thr * lu3_rpt);
+        if (lu3_thr == 128) launch_panel3<1, 128>(k0, kb, cl, gate_running, wk, invl);
+        else if constexpr (sizeof(T) == 8) launch_panel3<2, 256>(k0, kb, cl, gate_running, wk, invl);
+        else launch_panel3<1, 256>(k0, kb, cl, gate_running, wk, invl);
+        CPF_CUDA_CHECK(cudaEventRecord(evP, s));
+        // the next block lies in step k-1's "rest": wait for s2 to finish step k-1 (this also frees
+        // the gather/inv(L11) slot panel k+1 will write)
+        if (k > 0) CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evB, 0));
+        const int nb0 = k0 + kb, nb1 = std::min(nB, k0 + 2 * kb);
+        // s: next block only
+        lu_gather(slot, nb0, nb1, 0, 0, 0, s, gate_running);
+        lu_update_cols(k0, kb, nb0, nb1, invl, s, gate_running);
+        // s2: left columns + the rest + perm, after panel k
+        CPF_CUDA_CHECK(cudaStreamWaitEvent(s2, evP, 0));
+        lu_gather(slot, 0, k0, nb1, nB, 1, s2, gate_running);
+        lu_update_cols(k0, kb, nb1, nB, invl, s2, gate_running);
+        CPF_CUDA_CHECK(cudaEventRecord(evB, s2));
+      }
+      CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evB, 0));
+      launch(k_lu_info_to_err, 1, 1, 0, (const int*)lu.info, st);
+      ph_end();
+      return;
+    }
+    const int kbmax = lu_kb;
     for (int k0 = 0; k0 < nB; k0 += kbmax) {
       const int kb = std::min(kbmax, nB - k0);
       const int m = nB - k0;
-      if (lu3_rpt) {
-        const int cl = (m + lu3_thr * lu3_rpt - 1) / (lu3_thr * lu3_rpt);
-        if (lu3_thr == 128) launch_panel3<1, 128>(k0, kb, cl, gate_running);
-        else if constexpr (sizeof(T) == 8) launch_panel3<2, 256>(k0, kb, cl, gate_running);
-        else launch_panel3<1, 256>(k0, kb, cl, gate_running);
-      } else {
+      {
         int cl = lu_cl;
         const int rpc = (m + cl - 1) / cl;
         cudaLaunchConfig_t cfg{};
@@ -818,7 +891,6 @@ struct Engine final : EngineBase {
         ++nlaunch;
       }
       {
-        // always launched: block 0 also composes the panel interchange into perm
         const int cb = 256 / (2 * kLuMaxKB);
         const int ncols = nB - kb;
         launch(k_row_gather<T>, std::max(1u, nblocks(ncols, cb)), 256, 256 * sizeof(T), Phi, nB, nB, k0, kb, lu,
@@ -826,18 +898,10 @@ struct Engine final : EngineBase {
       }
       const int rest = nB - k0 - kb;
       if (rest > 0) {
-        if (lu3_rpt)
-          launch(k_u12<T, kLuMaxKB>, nblocks(rest, 64), 256, 0, Phi, nB, nB, k0, kb, (const T*)invL,
-                 (const LmDeviceState*)st, gate_running);
-        else
-          launch(k_trsm_llnu<T, kLuMaxKB>, nblocks(rest, 64), 64, 0, Phi, nB, nB, k0, kb, (const LmDeviceState*)st,
-                 gate_running);
-        if constexpr (sizeof(T) == 8)
-          launch(k_gemm_dmma, dim3(nblocks(rest, 64), nblocks(rest, 64)), 128, 0, Phi, nB, k0 + kb, k0 + kb, k0, rest,
-                 rest, kb, (const LmDeviceState*)st, gate_running);
-        else
-          launch(k_gemm_sub<T>, dim3(nblocks(rest, 64), nblocks(rest, 64)), 256, 0, Phi, nB, k0 + kb, k0 + kb, k0,
-                 rest, rest, kb, (const LmDeviceState*)st, gate_running);
+        launch(k_trsm_llnu<T, kLuMaxKB>, nblocks(rest, 64), 64, 0, Phi, nB, nB, k0, kb, (const LmDeviceState*)st,
+               gate_running);
+        launch(k_gemm_sub<T>, dim3(nblocks(rest, 64), nblocks(rest, 64)), 256, 0, Phi, nB, k0 + kb, k0 + kb, k0,
+               rest, rest, kb, (const LmDeviceState*)st, gate_running);
       }
     }
     launch(k_lu_info_to_err, 1, 1, 0, (const int*)lu.info, st);

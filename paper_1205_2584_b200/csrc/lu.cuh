@@ -231,6 +231,39 @@ __global__ void k_row_gather(T* __restrict__ A, int n, int lda, int k0, int kb, 
   if (do_perm) w.perm[w.gather[2 * e]] = pbuf[e];
 }
 
+// Row interchange restricted to the column ranges [ca0, ca1) U [cb0, cb1) (+ perm when do_perm):
+// the look-ahead LU applies it to the next block on one stream and to everything else on another.
+template <class T>
+__global__ void k_row_gather2(T* __restrict__ A, int lda, const int* __restrict__ gather, const int* __restrict__ gcount,
+                              int* __restrict__ perm, int ca0, int ca1, int cb0, int cb1, int do_perm,
+                              const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int G = *gcount;
+  if (G == 0) return;
+  T* buf = reinterpret_cast<T*>(smem_raw);
+  __shared__ int pbuf[2 * kLuMaxKB];
+  const int na = max(0, ca1 - ca0), nb = max(0, cb1 - cb0);
+  const int cb = blockDim.x / (2 * kLuMaxKB);
+  const int e = threadIdx.x % (2 * kLuMaxKB);
+  const int cl = threadIdx.x / (2 * kLuMaxKB);
+  const int cidx = blockIdx.x * cb + cl;
+  int col = -1;
+  if (cidx < na) col = ca0 + cidx;
+  else if (cidx < na + nb) col = cb0 + (cidx - na);
+  const bool do_col = (col >= 0) && (e < G);
+  T v = zero_of<T>();
+  if (do_col) v = A[(int64_t)gather[2 * e + 1] + (int64_t)lda * col];
+  const bool dp = do_perm && (blockIdx.x == 0) && (cl == 0) && (e < G);
+  int pv = 0;
+  if (dp) pv = perm[gather[2 * e + 1]];
+  buf[threadIdx.x] = v;
+  if (dp) pbuf[e] = pv;
+  __syncthreads();
+  if (do_col) A[(int64_t)gather[2 * e] + (int64_t)lda * col] = buf[threadIdx.x];
+  if (dp) perm[gather[2 * e]] = pbuf[e];
+}
+
 // U12 = L11^{-1} A12 (L11 unit lower, kb x kb); one thread per column of A12.
 template <class T, int KB>
 __global__ void k_trsm_llnu(T* __restrict__ A, int n, int lda, int k0, int kb, const LmDeviceState* st,

@@ -284,13 +284,14 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
 
 // U12 = inv(L11) A12 in place: CTA per 64-column tile of A12 (rows k0..k0+kb).
 template <class T, int KB>
-__global__ void __launch_bounds__(256) k_u12(T* __restrict__ A, int n, int lda, int k0, int kb,
-                                             const T* __restrict__ invL, const LmDeviceState* st, int gate_running) {
+__global__ void __launch_bounds__(256) k_u12(T* __restrict__ A, int cend, int lda, int k0, int kb,
+                                             const T* __restrict__ invL, const LmDeviceState* st, int gate_running,
+                                             int cbeg) {
   if (st && gate_running && (st->stopped || st->err_code)) return;
   __shared__ T Li[KB * KB];
   __shared__ T Bt[KB * 64];
-  const int c0 = k0 + kb + blockIdx.x * 64;
-  const int ncol = min(64, n - c0);
+  const int c0 = cbeg + blockIdx.x * 64;
+  const int ncol = min(64, cend - c0);
   for (int e = threadIdx.x; e < KB * KB; e += 256) Li[e] = invL[e];
   for (int e = threadIdx.x; e < KB * 64; e += 256) {
     const int i = e % KB, c = e / KB;
