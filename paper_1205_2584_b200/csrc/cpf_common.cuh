@@ -188,7 +188,8 @@ struct LmDeviceState {
   int max_iters;
   int cand_zero;             // normalised candidate had a zero-norm column (raise on accept)
   int err_direct;            // err/err_sq come from a direct residual (not the identity)
-  int pad_[2];
+  int force_direct;          // evaluate every trial fit directly (cheap-pass / LU-bound regime)
+  int pad_[1];
 };
 
 struct IterRecordDev {

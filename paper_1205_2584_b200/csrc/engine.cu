@@ -1119,6 +1119,16 @@ struct Engine final : EngineBase {
     hst->tol = tol;
     hst->max_iters = max_iters;
     hst->stopped = max_iters <= 0 ? kStopMaxIters : 0;
+    // When one direct-residual pass (2 J R flops) costs < 5% of the iteration's LU ((2/3) n_B^3),
+    // evaluate every trial fit directly from Y as well: removes the identity's ~eps/relerr^2
+    // cancellation error at no measurable cost (config 1 regime).
+    {
+      const double cw = sizeof(T) == 16 ? 4.0 : 1.0;
+      const double pass_flops = 2.0 * cw * (double)Jloc * world * R;
+      const double lu_flops = (2.0 / 3.0) * cw * (double)nB * nB * nB;
+      hst->force_direct = pass_flops < 0.05 * lu_flops ? 1 : 0;
+      if (const char* e = getenv("CPF_FORCE_DIRECT")) hst->force_direct = (e[0] == '1');
+    }
     // keep use_kinv computed by the cache kernels
     LmDeviceState tmp;
     CPF_CUDA_CHECK(cudaMemcpyAsync(&tmp, st, sizeof(tmp), cudaMemcpyDeviceToHost, s));

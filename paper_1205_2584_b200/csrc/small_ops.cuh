@@ -558,7 +558,7 @@ __global__ void k_precheck(const LmDeviceState* st, DevFlags* fl, const double* 
   const double scale_ = st->ynorm_sq + fabs(xx) + 2.0 * fabs(yx);
   const bool tiny = cs < 1e-10 * st->ynorm_sq;
   const bool close = fabs(st->err_sq - cs) <= 1e-12 * scale_;
-  fl->need_direct = (tiny || close) ? 1 : 0;
+  fl->need_direct = (tiny || close || st->force_direct) ? 1 : 0;
   fl->need_cur_direct = (fl->need_direct && !st->err_direct) ? 1 : 0;
 }
 
