@@ -192,10 +192,18 @@ struct Engine final : EngineBase {
     Jloc = Lrows * Cloc;
     nB = N * R * R;
     if ((int64_t)nB * nB > (int64_t)1 << 31) throw ApiError(CPF_E_UNSUPPORTED, "N*R^2 too large");
-    if (world > 1) {
-      if (!uid) throw ApiError(CPF_E_ARG, "world_size > 1 needs an NCCL unique id");
+    // CPF_FORCE_NCCL=1 runs a single-rank engine through the multi-rank code path (1-rank NCCL
+    // communicator, packed allreduce / allgather / reorder kernels) so it can be tested on 1 GPU.
+    const char* fe = getenv("CPF_FORCE_NCCL");
+    const bool force = fe && fe[0] == '1';
+    if (world > 1 || force) {
       ncclUniqueId id;
-      std::memcpy(&id, uid, sizeof(id));
+      if (world > 1) {
+        if (!uid) throw ApiError(CPF_E_ARG, "world_size > 1 needs an NCCL unique id");
+        std::memcpy(&id, uid, sizeof(id));
+      } else {
+        NCCL_CHECK(ncclGetUniqueId(&id));
+      }
       NCCL_CHECK(ncclCommInitRank(&comm, world, id, wrank));
     }
     alloc();
@@ -648,7 +656,7 @@ struct Engine final : EngineBase {
       CPF_CUDA_CHECK(cudaMemsetAsync(pa_out, 0, sizeof(T) * (I1 + Lmid) * R, s));
     }
   pass_a_done:
-    if (world > 1) {
+    if (comm) {
       NCCL_CHECK(ncclAllReduce(pa_out, pa_out, (size_t)(I1 + Lmid) * R * (sizeof(T) / sizeof(double)), ncclDouble,
                                ncclSum, comm, s));
     }
@@ -711,7 +719,7 @@ struct Engine final : EngineBase {
       });
     }
     ph_end();
-    if (world == 1) {
+    if (!comm) {
       launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, (const T*)bpart, Cloc, nparts, R, RP,
              IN, Mout + offs[N - 1], (const LmDeviceState*)st, (const DevFlags*)fl, gate);
     } else {
@@ -756,7 +764,7 @@ struct Engine final : EngineBase {
       launch(k_axpby<double>, 1, 1, 0, (const double*)out, 0.0, (const double*)nullptr, 0.0, out, (int64_t)1, cst, cfl,
              gate);
     }
-    if (world > 1) NCCL_CHECK(ncclAllReduce(out, out, 1, ncclDouble, ncclSum, comm, s));
+    if (comm) NCCL_CHECK(ncclAllReduce(out, out, 1, ncclDouble, ncclSum, comm, s));
   }
 
   // ------------------------------------------------------------------------------------------
@@ -996,7 +1004,7 @@ struct Engine final : EngineBase {
     } else {
       CPF_CUDA_CHECK(cudaMemsetAsync(dscal + 1, 0, sizeof(double), s));
     }
-    if (world > 1) NCCL_CHECK(ncclAllReduce(dscal + 1, dscal + 1, 1, ncclDouble, ncclSum, comm, s));
+    if (comm) NCCL_CHECK(ncclAllReduce(dscal + 1, dscal + 1, 1, ncclDouble, ncclSum, comm, s));
     double v;
     CPF_CUDA_CHECK(cudaMemcpyAsync(&v, dscal + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
     CPF_CUDA_CHECK(cudaStreamSynchronize(s));
