@@ -127,6 +127,9 @@ int cpf_engine_flm_step(cpf_engine* e, double mu, int variant, int refine_steps,
  * Phases: 0 pass A, 1 pass B, 2 LU factor, 3 solves, 4 other; counts = launches per phase. */
 int cpf_engine_profile(cpf_engine* e, int enable);
 int cpf_engine_phase_times(cpf_engine* e, double* ms_out, int64_t* counts_out, int nphases);
+/* G_n = Y_(n) Y_(n)^H (I_n x I_n, column-major) of the bound tensor, for the SVD initialisation
+ * (kruskal.py:227-242).  Sharded tensors: modes 1..N-1 only. */
+int cpf_engine_unfolding_gram(cpf_engine* e, int mode, void* out);
 /* Number of kernels this engine has launched (for the bench's gpu_launches count). */
 int64_t cpf_engine_launch_count(const cpf_engine* e);
 

@@ -76,6 +76,7 @@ EXPORTED_SYMBOLS = (
     "cpf_engine_profile",
     "cpf_engine_phase_times",
     "cpf_engine_launch_count",
+    "cpf_engine_unfolding_gram",
 )
 
 
@@ -121,6 +122,7 @@ def _declare(lib) -> None:
         "cpf_engine_profile": (I, [P, I]),
         "cpf_engine_phase_times": (I, [P, ctypes.POINTER(D), ctypes.POINTER(I64), I]),
         "cpf_engine_launch_count": (I64, [P]),
+        "cpf_engine_unfolding_gram": (I, [P, I, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -292,6 +294,12 @@ class Engine:
         cnt = (ctypes.c_int64 * n)()
         self._check(self._lib.cpf_engine_phase_times(self._h, ms, cnt, n))
         return list(ms), list(cnt)
+
+    def unfolding_gram(self, mode: int) -> np.ndarray:
+        d = self.dims[mode - 1] if mode < len(self.dims) else (self.slab[1] - self.slab[0])
+        out = np.empty((d, d), dtype=self.dtype, order="F")
+        self._check(self._lib.cpf_engine_unfolding_gram(self._h, int(mode), out.ctypes.data))
+        return out
 
     def launch_count(self) -> int:
         return int(self._lib.cpf_engine_launch_count(self._h))

@@ -71,6 +71,7 @@ struct EngineBase {
   virtual void profile(int on) = 0;
   virtual void phase_times(double* ms, int64_t* cnt, int n) = 0;
   virtual int64_t launches() const = 0;
+  virtual void unfolding_gram(int mode, void* out) = 0;
 };
 
 template <class T>
@@ -1290,6 +1291,35 @@ struct Engine final : EngineBase {
     }
   }
   int64_t launches() const override { return nlaunch; }
+
+  // G_n = Y_(n) Y_(n)^H on the device (sum of the slab partials across ranks for n < N)
+  void unfolding_gram(int mode, void* out) override {
+    if (!have_tensor) throw ApiError(CPF_E_STATE, "no tensor bound");
+    if (mode < 1 || mode > N) throw ApiError(CPF_E_ARG, "mode out of range");
+    if (mode == N && world > 1) throw ApiError(CPF_E_UNSUPPORTED, "mode-N Gram of a sharded tensor");
+    const int n = mode - 1;
+    int64_t P = 1, Q = 1;
+    for (int k = 0; k < n; ++k) P *= dims[k];
+    for (int k = n + 1; k < N; ++k) Q *= (k == N - 1) ? Cloc : dims[k];
+    const int64_t In = (n == N - 1) ? Cloc : dims[n];
+    const int64_t K = P * Q;
+    const int ntile = (int)((In + 31) / 32);
+    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>((K + 4095) / 4096, (148 * 8) / std::max(1, ntile * ntile) + 1));
+    const int64_t kchunk = ((K + nsplit - 1) / nsplit + 31) / 32 * 32;
+    nsplit = (int)((K + kchunk - 1) / kchunk);
+    T* part = nullptr;
+    T* G = nullptr;
+    CPF_CUDA_CHECK(cudaMalloc(&part, sizeof(T) * (size_t)nsplit * In * In));
+    CPF_CUDA_CHECK(cudaMalloc(&G, sizeof(T) * (size_t)In * In));
+    launch(k_unfold_gram<T>, dim3(ntile * ntile, nsplit), 256, 0, Y, P, In, Q, kchunk, part);
+    launch(k_gram_reduce<T>, nblocks(In * In, 256), 256, 0, (const T*)part, nsplit, In * In, G);
+    if (comm && mode < N)
+      NCCL_CHECK(ncclAllReduce(G, G, (size_t)In * In * (sizeof(T) / sizeof(double)), ncclDouble, ncclSum, comm, s));
+    CPF_CUDA_CHECK(cudaMemcpyAsync(out, G, sizeof(T) * In * In, cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    cudaFree(part);
+    cudaFree(G);
+  }
 };
 
 }  // namespace cpf
@@ -1440,6 +1470,11 @@ int cpf_engine_phase_times(cpf_engine* e, double* ms_out, int64_t* counts_out, i
 }
 
 int64_t cpf_engine_launch_count(const cpf_engine* e) { return (e && e->impl) ? e->impl->launches() : 0; }
+
+int cpf_engine_unfolding_gram(cpf_engine* e, int mode, void* out) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->unfolding_gram(mode, out); });
+}
 
 }  // extern "C"
 

@@ -368,3 +368,73 @@ __global__ void k_z_reduce(const T* __restrict__ z_part, int ntiles, int64_t Lmi
 }
 
 }  // namespace cpf
+
+namespace cpf {
+
+// Unfolding Gram G_n = Y_(n) Y_(n)^H (I_n x I_n) for the SVD initialisation (kruskal.py:227-242:
+// the leading left singular vectors of Y_(n) are the leading eigenvectors of G_n).
+// Y_(n)[i, k] with k = a + P b  ->  Y[a + P i + P I_n b]  (a over modes < n, b over modes > n).
+// grid (tiles_i * tiles_i, ksplit); 32x32 output tile per CTA, 256 threads x (2x2); per-CTA partial
+// tiles are summed by k_gram_reduce in fixed order.
+template <class T>
+__global__ void __launch_bounds__(256) k_unfold_gram(const T* __restrict__ Y, int64_t P, int64_t In, int64_t Q,
+                                                     int64_t kchunk, T* __restrict__ part) {
+  __shared__ T As[32][33];
+  __shared__ T Bs[32][33];
+  const int ntile = (int)((In + 31) / 32);
+  const int ti = blockIdx.x % ntile, tj = blockIdx.x / ntile;
+  const int64_t K = P * Q;
+  const int64_t kbeg = (int64_t)blockIdx.y * kchunk, kend = min(K, kbeg + kchunk);
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  T acc[2][2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) acc[u][v] = zero_of<T>();
+  for (int64_t k0 = kbeg; k0 < kend; k0 += 32) {
+    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+      int kk, ii;
+      if (P == 1) { ii = e % 32; kk = e / 32; } else { kk = e % 32; ii = e / 32; }
+      const int64_t k = k0 + kk;
+      const int64_t gi = (int64_t)ti * 32 + ii, gj = (int64_t)tj * 32 + ii;
+      T va = zero_of<T>(), vb = zero_of<T>();
+      if (k < kend) {
+        const int64_t a = k % P, b = k / P;
+        const int64_t base = a + P * In * b;
+        if (gi < In) va = Y[base + P * gi];
+        if (gj < In) vb = Y[base + P * gj];
+      }
+      As[kk][ii] = va;
+      Bs[kk][ii] = vb;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      const T a0 = As[kk][ty], a1 = As[kk][ty + 16];
+      const T b0 = cj(Bs[kk][tx]), b1 = cj(Bs[kk][tx + 16]);
+      fma_acc(acc[0][0], a0, b0);
+      fma_acc(acc[0][1], a0, b1);
+      fma_acc(acc[1][0], a1, b0);
+      fma_acc(acc[1][1], a1, b1);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int64_t gi = (int64_t)ti * 32 + ty + 16 * u, gj = (int64_t)tj * 32 + tx + 16 * v;
+      if (gi < In && gj < In) part[((int64_t)blockIdx.y * In + gj) * In + gi] = acc[u][v];  // column-major
+    }
+}
+
+template <class T>
+__global__ void k_gram_reduce(const T* __restrict__ part, int nsplit, int64_t n2, T* __restrict__ G) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n2) return;
+  T s = part[e];
+  for (int q = 1; q < nsplit; ++q) s = add(s, part[(int64_t)q * n2 + e]);
+  G[e] = s;
+}
+
+}  // namespace cpf

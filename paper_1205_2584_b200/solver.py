@@ -96,12 +96,59 @@ class _Dims:
         self.dims, self.scalar_kind = tuple(dims), kind
 
 
-def _init_model(y, config: FitConfig, rng) -> KruskalModel:
+def _init_model(y, config: FitConfig, rng, eng=None) -> KruskalModel:
     if config.init == "random":
         return random_init(y.dims, config.rank, rng, y.scalar_kind)
     if config.init == "svd":
-        raise ValueError("init='svd' is not supported on the B200 backend yet; use init='random'")
+        if eng is None:
+            raise ValueError("init='svd' needs the tensor bound to the engine")
+        return svd_init(eng, y.dims, config.rank, rng, y.scalar_kind)
     raise ValueError(f"unknown init {config.init!r}")
+
+
+def _eigh_descending(g: np.ndarray):
+    """Eigen-decomposition of a small Hermitian Gram on the GPU (cuSOLVER through torch) when
+    available; eigenvalues descending."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            w, v = torch.linalg.eigh(torch.from_numpy(np.ascontiguousarray(g)).cuda())
+            w, v = w.cpu().numpy(), v.cpu().numpy()
+        else:  # pragma: no cover - the engine itself needs a GPU
+            w, v = np.linalg.eigh(g)
+    except ImportError:  # pragma: no cover
+        w, v = np.linalg.eigh(g)
+    return w[::-1], v[:, ::-1]
+
+
+def svd_init(eng, dims, rank: int, rng, scalar_kind: str = "real") -> KruskalModel:
+    """Leading mode-n left singular vectors (kruskal.py:227-242), computed as the leading
+    eigenvectors of the unfolding Gram Y_(n) Y_(n)^H formed on the GPU (cpf_engine_unfolding_gram);
+    extra columns (R > rank of the unfolding) are unit-norm draws from ``rng`` exactly as in the
+    reference.  Singular vectors are only defined up to sign/phase: each column is normalised so its
+    largest-magnitude entry is real positive (LAPACK's gesdd convention is implementation-defined)."""
+    total = int(np.prod(dims, dtype=np.int64))
+    factors = []
+    for n, d in enumerate(dims):
+        g = eng.unfolding_gram(n + 1)
+        g = 0.5 * (g + g.conj().T)
+        _, v = _eigh_descending(g)
+        k = min(rank, d, total // d)
+        u = np.array(v[:, :k])
+        for r in range(k):
+            top = u[np.argmax(np.abs(u[:, r])), r]
+            u[:, r] = u[:, r] / (top / abs(top))
+        cols = [u]
+        if k < rank:
+            extra = rng.standard_normal((d, rank - k))
+            if scalar_kind == COMPLEX:
+                extra = extra + 1j * rng.standard_normal(extra.shape)
+            extra = extra / np.linalg.norm(extra, axis=0, keepdims=True)
+            cols.append(extra.astype(u.dtype))
+        dtype = np.complex128 if scalar_kind == COMPLEX else np.float64
+        factors.append(np.hstack(cols).astype(dtype))
+    return KruskalModel(factors)
 
 
 def _stop_reason(st) -> str:
@@ -175,9 +222,11 @@ def fit(y, config: FitConfig, *, device=None, distributed=None, slab_of=None) ->
     y = as_dense(y)
     gdims = y.dims if slab_of is None else tuple(y.dims[:-1]) + (int(slab_of),)
     rng = np.random.default_rng([config.seed, 0])
-    init = _init_model(_Dims(gdims, y.scalar_kind), config, rng)
+    if config.init not in ("svd", "random"):
+        raise ValueError(f"unknown init {config.init!r}")
     eng = _make_engine(y, config.rank, device, distributed, slab_of)
     try:
+        init = _init_model(_Dims(gdims, y.scalar_kind), config, rng, eng)
         eng.set_factors(init.as_vector())
         st = eng.fit_begin(config.variant, config.tau, config.tol, config.max_iters)
         while st.stopped == _native.STOP_RUNNING:

@@ -196,3 +196,47 @@ def test_fit_large_mode1_matches_oracle(api):
     assert "".join("A" if r.accepted else "r" for r in res.trace) == ref.accepted
     assert abs(res.final_relerr - ref.final_relerr) < FIT_ATOL
     assert _rel(res.model.as_vector(), O.stack(ref.factors)) < FACTOR_RTOL
+
+
+# ---- the reference's default init="svd" (kruskal.py:227-242), GPU unfolding Grams
+@pytest.mark.parametrize("variant", ["auto", "flm-a"])
+def test_svd_init_converges_on_exact_instance(api, variant):
+    # mirrors the reference's test_converges_on_exact_instance (default FitConfig: init="svd")
+    rng = np.random.default_rng(14)
+    fac = [rng.standard_normal((8, 2)) for _ in range(3)]
+    for f in fac:
+        f /= np.linalg.norm(f, axis=0, keepdims=True)
+    from oracle import cp_oracle as O
+
+    y = api.DenseTensor(O.reconstruct(fac))
+    res = api.fit(y, api.FitConfig(rank=2, variant=variant, seed=3, max_iters=300))
+    assert res.final_relerr < 1e-8
+    assert res.stop_reason == "tol"
+    assert res.iters >= res.accepted_iters >= 1
+
+
+@pytest.mark.parametrize("dims,rank,cplx", [((6, 7, 8), 3, False), ((5, 4, 6), 2, True), ((3, 4, 2, 5), 4, False),
+                                            ((520, 6, 5), 4, False)])
+def test_unfolding_gram_and_svd_subspace(api, dims, rank, cplx):
+    from oracle import cp_oracle as O
+    from paper_1205_2584_b200 import _native
+    from paper_1205_2584_b200.solver import svd_init
+
+    rng = np.random.default_rng(sum(dims))
+    y = rng.standard_normal(dims) + (1j * rng.standard_normal(dims) if cplx else 0)
+    y = np.asfortranarray(y)
+    eng = _native.Engine(_native.CPF_COMPLEX if cplx else _native.CPF_REAL, dims, rank)
+    try:
+        eng.set_tensor_host(y)
+        for n in range(1, len(dims) + 1):
+            u = O.unfold(y, n)
+            assert _rel(eng.unfolding_gram(n), u @ u.conj().T) < 1e-13
+        model = svd_init(eng, dims, rank, np.random.default_rng(0), "complex" if cplx else "real")
+    finally:
+        eng.close()
+    for n, f in enumerate(model.factors):
+        u, _, _ = np.linalg.svd(O.unfold(y, n + 1), full_matrices=False)
+        k = min(rank, u.shape[1])
+        # same leading subspace as the reference's svd_init (up to column signs / phases)
+        proj = np.abs(u[:, :k].conj().T @ f[:, :k])
+        np.testing.assert_allclose(np.diag(proj), 1.0, atol=1e-8)

@@ -57,6 +57,13 @@ def test_non_lm_variants_rejected_before_any_device_work():
             fit(y, FitConfig(rank=1, variant=v, init="random"))
 
 
+def test_unknown_init_rejected():
+    from paper_1205_2584_b200 import DenseTensor, FitConfig, fit
+
+    with pytest.raises(ValueError):
+        fit(DenseTensor(np.ones((3, 3, 3))), FitConfig(rank=1, init="nope"))
+
+
 def test_fit_complex_kind_check():
     from paper_1205_2584_b200 import DenseTensor, FitConfig, fit_complex
 
