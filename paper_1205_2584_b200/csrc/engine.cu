@@ -86,6 +86,9 @@ struct Engine final : EngineBase {
   Modes md{};
   MidGeom mg{};
   cudaStream_t s = nullptr;
+  cudaStream_t ls = nullptr;   // stream the launch helpers target (s, or s3 for the overlapped pass B)
+  cudaStream_t s3 = nullptr;   // pass B + gradient of an accepted step, overlapped with the next LU
+  cudaEvent_t evF = nullptr, evG = nullptr;
   ncclComm_t comm = nullptr;
   int64_t nlaunch = 0;
 
@@ -167,6 +170,10 @@ struct Engine final : EngineBase {
     wrank = wr;
     CPF_CUDA_CHECK(cudaSetDevice(dev));
     CPF_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CPF_CUDA_CHECK(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
+    CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evF, cudaEventDisableTiming));
+    CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evG, cudaEventDisableTiming));
+    ls = s;
     for (int n = 0; n < N; ++n) {
       if (d[n] < 1) throw ApiError(CPF_E_ARG, "dims must be >= 1");
       dims[n] = d[n];
@@ -219,6 +226,9 @@ struct Engine final : EngineBase {
     if (evB) cudaEventDestroy(evB);
     if (evJ) cudaEventDestroy(evJ);
     if (s2) cudaStreamDestroy(s2);
+    if (evF) cudaEventDestroy(evF);
+    if (evG) cudaEventDestroy(evG);
+    if (s3) cudaStreamDestroy(s3);
     for (auto& e : evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     void* ptrs[] = {Yown, A, Ac, M, Mc, D, G, Cand, V1, V2, V3, V4, Cg, Ccg, Gx, Gp, Gf, Gti, Gi, W1, Sm,
                     wvec, fvec, xvec, Phi, A1c, KMc, WNc, A1r, KMr, WNr, zpart, m1part, bpart, pa_out, pb_out, pb_all,
@@ -524,7 +534,7 @@ struct Engine final : EngineBase {
   template <class K, class... Args>
   void launch(K kern, dim3 g, dim3 b, size_t smem, Args... args) {
     if (g.x == 0 || g.y == 0 || g.z == 0) return;
-    kern<<<g, b, smem, s>>>(args...);
+    kern<<<g, b, smem, ls>>>(args...);
     ++nlaunch;
     CPF_CUDA_CHECK(cudaGetLastError());
   }
@@ -536,7 +546,7 @@ struct Engine final : EngineBase {
     if (!prof) return;
     cudaEvent_t a;
     CPF_CUDA_CHECK(cudaEventCreate(&a));
-    CPF_CUDA_CHECK(cudaEventRecord(a, s));
+    CPF_CUDA_CHECK(cudaEventRecord(a, ls));
     cur_phase = ph;
     cur_ev = a;
   }
@@ -544,7 +554,7 @@ struct Engine final : EngineBase {
     if (!prof || cur_phase < 0) return;
     cudaEvent_t b;
     CPF_CUDA_CHECK(cudaEventCreate(&b));
-    CPF_CUDA_CHECK(cudaEventRecord(b, s));
+    CPF_CUDA_CHECK(cudaEventRecord(b, ls));
     evs.push_back({cur_phase, cur_ev, b});
     cur_phase = -1;
   }
@@ -724,12 +734,12 @@ struct Engine final : EngineBase {
       launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, (const T*)bpart, Cloc, nparts, R, RP,
              IN, Mout + offs[N - 1], (const LmDeviceState*)st, (const DevFlags*)fl, gate);
     } else {
-      CPF_CUDA_CHECK(cudaMemsetAsync(pb_out, 0, sizeof(T) * Cpad * R, s));
+      CPF_CUDA_CHECK(cudaMemsetAsync(pb_out, 0, sizeof(T) * Cpad * R, ls));
       if (Cloc > 0)
         launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, (const T*)bpart, Cloc, nparts, R, RP,
                Cpad, pb_out, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
       const size_t cnt = (size_t)Cpad * R * (sizeof(T) / sizeof(double));
-      NCCL_CHECK(ncclAllGather(pb_out, pb_all, cnt, ncclDouble, comm, s));
+      NCCL_CHECK(ncclAllGather(pb_out, pb_all, cnt, ncclDouble, comm, ls));
       // pb_all[rank][c + Cpad r] -> Mout_N[(rank*Cpad + c) + IN r]
       for (int q = 0; q < world; ++q) {
         const int64_t lo = std::min<int64_t>(IN, (int64_t)q * Cpad);
@@ -935,19 +945,25 @@ struct Engine final : EngineBase {
   }
 
   // fLM candidate at (A, cache, M, G) with the state's mu -> Cand  (solver.py:189-226)
-  void candidate(int refine_steps, int gate) {
+  // Damped Gamma inverses for the state's mu, Phi and its LU: everything of the step that does
+  // not depend on Y or the MTTKRPs (it only needs the Grams and mu)
+  void prepare_core(int gate) {
     const int gr = gate == kRunning ? 1 : 0;
     launch(k_damped_inverses<T>, 2 * N, 128, 2 * R * R * sizeof(T), (const T*)Gx, N, R, Gti, Gi, st,
            (const DevFlags*)fl, gate, (const int*)kinv_ok, (const double*)nullptr);
+    launch(k_phi_assemble<T>, nblocks((int64_t)nB * nB, 256), 256, 0, Phi, N, R, (const T*)Cg, (const T*)Gi,
+           (const T*)Gp, (const T*)Gf, (const LmDeviceState*)st, gr);
+    lu_factor(gr);
+  }
+
+  void candidate(int refine_steps, int gate, bool core_ready = false) {
+    const int gr = gate == kRunning ? 1 : 0;
+    if (!core_ready) prepare_core(gate);
     // damped factors D = M Gti
     { TallArgs a{}; a.X1 = M; a.S1 = Gti; a.s1stride = (int64_t)R * R; a.out = D; tall(a, gate); }
     // w = vec(A^H D - C Gamma^T Gti)
     cross_gram(A, D, W1, gate);
     small(kOpW, W1, Cg, wvec, gate);
-    // core system
-    launch(k_phi_assemble<T>, nblocks((int64_t)nB * nB, 256), 256, 0, Phi, N, R, (const T*)Cg, (const T*)Gi,
-           (const T*)Gp, (const T*)Gf, (const LmDeviceState*)st, gr);
-    lu_factor(gr);
     apply_b(wvec, fvec, gr);
     // update: Cand = D + A (I - (F + Gamma^T) Gti)
     small(kOpE, fvec, nullptr, Sm, gate);
@@ -1144,6 +1160,7 @@ struct Engine final : EngineBase {
     CPF_CUDA_CHECK(cudaStreamSynchronize(s));
     hst->use_kinv = tmp.use_kinv;
     CPF_CUDA_CHECK(cudaMemcpyAsync(st, hst, sizeof(LmDeviceState), cudaMemcpyHostToDevice, s));
+    prepare_core(kRunning);  // Phi(mu_0, cache_0) for the first iteration
     CPF_CUDA_CHECK(cudaStreamSynchronize(s));
     fill_status(o);
   }
@@ -1152,7 +1169,7 @@ struct Engine final : EngineBase {
 
   void iteration() {
     const int g = kRunning;
-    candidate(2, g);
+    candidate(2, g, /*core_ready=*/true);  // Phi(mu_t, cache_t) was factored at the end of t-1
     // delta' = cand - model (solver.py:348)
     axpby(Cand, 1.0, A, -1.0, V1, g);
     // normalised candidate: trial fit and, if accepted, the new model (solver.py:362)
@@ -1176,8 +1193,17 @@ struct Engine final : EngineBase {
     cache_from_grams(Cg, ga);
     launch(k_copy<T>, nblocks(offs[N - 1], 256), 256, 0, (const T*)Mc, M, offs[N - 1], (const LmDeviceState*)st,
            (const DevFlags*)fl, ga);
+    // fork: pass B (M_N of the new model) + gradient on s3, while s factors the next step's
+    // core system Phi(mu_{t+1}, cache_{t+1}) -- independent of Y, so the two overlap
+    CPF_CUDA_CHECK(cudaEventRecord(evF, s));
+    CPF_CUDA_CHECK(cudaStreamWaitEvent(s3, evF, 0));
+    ls = s3;
     pass_b(A, M, ga);
     gradient(ga);
+    ls = s;
+    CPF_CUDA_CHECK(cudaEventRecord(evG, s3));
+    prepare_core(g);
+    CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evG, 0));
     launch(k_clear_pending, 1, 1, 0, fl);
   }
 
