@@ -169,8 +169,10 @@ struct Engine final : EngineBase {
     world = ws;
     wrank = wr;
     CPF_CUDA_CHECK(cudaSetDevice(dev));
-    CPF_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    CPF_CUDA_CHECK(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
+    int prio_lo = 0, prio_hi = 0;
+    CPF_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    CPF_CUDA_CHECK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio_hi));
+    CPF_CUDA_CHECK(cudaStreamCreateWithPriority(&s3, cudaStreamNonBlocking, prio_lo));
     CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evF, cudaEventDisableTiming));
     CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evG, cudaEventDisableTiming));
     ls = s;
@@ -286,9 +288,12 @@ struct Engine final : EngineBase {
   }
 
   // Launch geometry for the tensor passes and the LU panel.
+  int nsm_ = 148;
+  static constexpr int kLuReserveSms = 20;  // SMs left to the LU while pass B runs alongside it
   void plan() {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    nsm_ = nsm;
     const size_t es = sizeof(T);
     // pass A: threads sized so 2*threads*RP*es (+W stage) fits ~160 KB
     pa_threads = 256;
@@ -343,7 +348,11 @@ struct Engine final : EngineBase {
   void plan_lu3() {
     invL = dalloc<T>(2 * kLuMaxKB * kLuMaxKB);
     gring = dalloc<int>(2 * (4 * kLuMaxKB + 4));
-    CPF_CUDA_CHECK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    {
+      int plo = 0, phi = 0;
+      CPF_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&plo, &phi));
+      CPF_CUDA_CHECK(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, phi));
+    }
     CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evP, cudaEventDisableTiming));
     CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
     CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evJ, cudaEventDisableTiming));
@@ -390,6 +399,7 @@ struct Engine final : EngineBase {
   void set_dmma_attrs() {
     CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_dmma<NT, 0, kDmmaCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)da_smem));
     CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_dmma<NT, 1, kDmmaCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)db_smem));
+    CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pass_b_dmma_pers<NT, kDmmaCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)db_smem));
   }
   template <class F>
   void dispatch_nt(F&& f) {
@@ -700,9 +710,17 @@ struct Engine final : EngineBase {
           launch(k_krmid<T>, nblocks(Lmid * db.WS, 256), 256, 0, F, mg, Lmid, R, db.WS, (T*)KMd, cst, cfl, gate, 1);
         dispatch_nt([&](auto ntc) {
           constexpr int NTc = decltype(ntc)::value;
-          launch(k_pass_dmma<NTc, 1, kDmmaCK>, dim3(db.tiles, (unsigned)Cloc, db_chunks), dim3(kConsumers + 32), db_smem,
-                 (const double*)Y, db, (const double*)KMd, (const double*)A1c, (const double*)KMc, RP, R, (double*)zpart,
-                 (double*)bpart, cst, cfl, gate);
+          if (ls != s && getenv("CPF_PERSISTENT_B")) {
+            // overlapped with the next LU: persistent grid that leaves SMs for the panel cluster
+            const int64_t items = (int64_t)db.tiles * Cloc * db_chunks;
+            const int ctas = (int)std::min<int64_t>(items, std::max(1, nsm_ - kLuReserveSms));
+            launch(k_pass_b_dmma_pers<NTc, kDmmaCK>, dim3(ctas), dim3(kConsumers + 32), db_smem, (const double*)Y, db,
+                   (const double*)KMd, (const double*)A1c, RP, R, (int)Cloc, db_chunks, (double*)bpart, cst, cfl, gate);
+          } else {
+            launch(k_pass_dmma<NTc, 1, kDmmaCK>, dim3(db.tiles, (unsigned)Cloc, db_chunks), dim3(kConsumers + 32), db_smem,
+                   (const double*)Y, db, (const double*)KMd, (const double*)A1c, (const double*)KMc, RP, R, (double*)zpart,
+                   (double*)bpart, cst, cfl, gate);
+          }
         });
         done_b = true;
       }
