@@ -2,6 +2,7 @@
 
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -25,16 +26,28 @@ def sources():
     return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "cpfast_b200.h"]
 
 
+STAMP = OUT.with_suffix(".srchash")
+
+
+def source_hash() -> str:
+    """Content hash of every source the library is built from (mtimes do not survive snapshots)."""
+    h = hashlib.sha256()
+    for p in sources():
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()
+
+
 def up_to_date() -> bool:
-    if not OUT.exists():
+    if not OUT.exists() or not STAMP.exists():
         return False
-    t = OUT.stat().st_mtime
-    return all(p.stat().st_mtime <= t for p in sources())
+    return STAMP.read_text().strip() == source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return OUT
+    digest = source_hash()
     OUT.parent.mkdir(parents=True, exist_ok=True)
     tmp = OUT.with_suffix(".so.tmp")
     cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
@@ -47,6 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if verbose:
         sys.stderr.write(res.stderr)
     os.replace(tmp, OUT)
+    STAMP.write_text(digest + "\n")
     return OUT
 
 
