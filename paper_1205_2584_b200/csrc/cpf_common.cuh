@@ -252,6 +252,13 @@ __device__ __forceinline__ void st_cluster(uint32_t addr, double v) {
 __device__ __forceinline__ void st_cluster(uint32_t addr, cplx v) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
 }
+// 16-byte remote store that completes 16 tx-bytes on the destination CTA's mbarrier (st.async):
+// the receiver learns the data has landed by waiting on its own local mbarrier, no cluster barrier.
+__device__ __forceinline__ void st_async16(uint32_t raddr, double x, double y, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr), "d"(x),
+               "d"(y), "r"(rbar)
+               : "memory");
+}
 __device__ __forceinline__ void st_cluster(uint32_t addr, int v) {
   asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }

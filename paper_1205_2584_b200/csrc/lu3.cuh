@@ -1,10 +1,12 @@
 // LU v3 building blocks (see lu.cuh for the algorithm outline and the solves).
 //
-// k_panel_lu3: the m x KB panel lives in REGISTERS: a thread-block cluster of CL CTAs x 256
-// threads, each thread owning RPT rows (KB values each).  Per column: warp-level argmax ->
-// the warp's candidate row is broadcast into every CTA's shared memory (DSMEM) -> ONE cluster
-// barrier -> every warp picks the winner from the NC = CL*8 candidates -> rank-1 elimination of
-// the thread's own rows in registers.  Pivot rows are pivoted logically (retired) and written
+// k_panel_lu3: the m x KB panel lives in REGISTERS: a thread-block cluster of CL CTAs x NTHR
+// threads, each thread owning RPT rows (KB values each).  Per column: warp argmax -> CTA argmax
+// (one __syncthreads) -> the CTA's candidate packet (row, |pivot|, row index, 1/pivot) is pushed
+// into every CTA's shared memory with st.async, each 16-byte store completing tx-bytes on the
+// receiver's mbarrier -> every CTA waits on its OWN mbarrier (no cluster barrier: cluster.sync
+// costs a GPU-scope fence + L1 invalidate per column) -> winner among the CL packets -> rank-1
+// elimination of the thread's own rows in registers.  Pivot rows are pivoted logically (retired) and written
 // once at the end; the panel's interchange is emitted as a gather list and inv(L11) is produced
 // for the U12 = inv(L11) A12 update (k_u12).
 // k_gemm_dmma: trailing update A22 -= L21 U12 on the fp64 tensor cores (mma.sync m8n8k4.f64,
@@ -28,15 +30,33 @@ __device__ __forceinline__ cplx shfl_val<cplx>(cplx v, int src) {
   return cplx{__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src)};
 }
 
+// Candidate packet one CTA pushes into every CTA of the cluster per column: the candidate row
+// (KB elements), then {|pivot|, row} and {1/pivot} -- 16-byte chunks, pushed by all NTHR threads
+// of the CTA (ceil(CL * PKC / NTHR) st.async each).
+template <class T, int KB>
+struct PanelPacket {
+  static constexpr int DC = KB * (int)sizeof(T) / 16;  // data chunks
+  static constexpr int PKC = DC + 2;                   // + key chunk + reciprocal chunk
+};
+
 template <class T>
 size_t panel3_smem_bytes(int CL, int KB, int nthr) {
-  const size_t NC = (size_t)CL;  // one candidate per CTA
   const size_t NW = (size_t)nthr / 32;
-  size_t b = sizeof(T) * (2 * NC * KB + (size_t)KB * KB + NW * KB + 2 * NC);  // + rcp slots
-  b += sizeof(double) * 2 * NC + sizeof(int) * 2 * NC + sizeof(int) * 4 * KB;
-  b += sizeof(double) * NW + sizeof(int) * NW;  // per-warp keys
+  const size_t NC = (size_t)CL;  // one published candidate per CTA
+  const size_t pkc = (size_t)KB * sizeof(T) / 16 + 2;
+  size_t b = 16 + 16 * 2 * NC * pkc + sizeof(T) * ((size_t)KB * KB + NW * KB);  // 2 mbarriers first
+  b += sizeof(double) * NW + sizeof(int) * NW + sizeof(int) * 4 * KB;
   return (b + 15) & ~(size_t)15;
 }
+
+__device__ __forceinline__ double2 as_d2(double v) { return make_double2(v, 0.0); }
+__device__ __forceinline__ double2 as_d2(cplx v) { return make_double2(v.x, v.y); }
+template <class T>
+__device__ __forceinline__ T from_d2(double2 v);
+template <>
+__device__ __forceinline__ double from_d2<double>(double2 v) { return v.x; }
+template <>
+__device__ __forceinline__ cplx from_d2<cplx>(double2 v) { return cplx{v.x, v.y}; }
 
 // Warp argmax of non-negative doubles with ties broken by the smaller row (redux-based: 3
 // warp reductions instead of a 5-round shuffle tree).  Returns the winning value/row/lane.
@@ -61,17 +81,15 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
   const int rank = (int)cluster.block_rank();
   constexpr int NW = NTHR / 32;
   const int NC = CL;  // one published candidate per CTA
+  using PK = PanelPacket<T, KB>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* cand_data = reinterpret_cast<T*>(smem_raw);            // [2][NC][KB]
-  T* top = cand_data + (size_t)2 * NC * KB;                  // [KB][KB] row jj = pivot row jj
+  uint64_t* pbar = reinterpret_cast<uint64_t*>(smem_raw);    // [2] packet-arrival mbarriers (by parity)
+  double2* cand_pk = reinterpret_cast<double2*>(smem_raw + 16);  // [2][NC][PKC] packets pushed by every CTA
+  T* top = reinterpret_cast<T*>(cand_pk + (size_t)2 * NC * PK::PKC);  // [KB][KB] row jj = pivot row jj
   T* wrow_s = top + (size_t)KB * KB;                         // [NW][KB] staging of each warp's candidate
-  T* cand_rcp = wrow_s + (size_t)NW * KB;                    // [2][NC] 1/pivot of each candidate
-  T* wrcp = cand_rcp + 2 * NC;                               // [NW] 1/pivot of each warp candidate
-  double* wkey_v = reinterpret_cast<double*>(wrcp + NW);     // [NW]
+  double* wkey_v = reinterpret_cast<double*>(wrow_s + (size_t)NW * KB);  // [NW]
   int* wkey_r = reinterpret_cast<int*>(wkey_v + NW);               // [NW]
-  double* cand_val = reinterpret_cast<double*>(wkey_r + NW);
-  int* cand_row = reinterpret_cast<int*>(cand_val + 2 * NC);
-  int* pivrows = cand_row + 2 * NC;                          // [KB]
+  int* pivrows = wkey_r + NW;                                // [KB]
   int* Dl = pivrows + KB;                                    // [KB]
   int* Vl = Dl + KB;                                         // [KB]
   int* misc = Vl + KB;                                       // [KB]
@@ -90,19 +108,18 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
 #pragma unroll
     for (int q = 0; q < KB; ++q) a[j][q] = (alive[j] && q < kb) ? src[(int64_t)lda * q] : zero_of<T>();
   }
-  // DSMEM bases of the candidate slots in every CTA of the cluster (same layout everywhere)
-  uint32_t rbase_data[16], rbase_val[16], rbase_row[16], rbase_rcp[16];
-#pragma unroll
-  for (int r = 0; r < 16; ++r)
-    if (r < CL) {
-      rbase_data[r] = mapa_u32(cand_data, r);
-      rbase_val[r] = mapa_u32(cand_val, r);
-      rbase_row[r] = mapa_u32(cand_row, r);
-      rbase_rcp[r] = mapa_u32(cand_rcp, r);
-    }
   T cur[RPT];  // a[j][jj] of the current column, maintained by the elimination loop
 #pragma unroll
   for (int j = 0; j < RPT; ++j) cur[j] = a[j][0];
+  // packet exchange: every CTA pushes its candidate into every CTA with st.async; pbar[par]
+  // completes when all CL packets of the column have landed (tx = CL * PKC * 16 bytes)
+  if (tid == 0) {
+    mbar_init(&pbar[0], 1);
+    mbar_init(&pbar[1], 1);
+    fence_mbar_init();
+  }
+  cluster.sync();  // remote CTAs may target pbar only once it is initialised
+  const uint32_t pk_tx = (uint32_t)(NC * PK::PKC * 16);
 
   // Column loop NOT unrolled (I-cache); registers addressed statically by predication over q.
 #ifdef CPF_PANEL_TIMING
@@ -143,44 +160,46 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
       wkey_r[wid] = wrow;
     }
     __syncthreads();
-    // ---- (c) warp 0: CTA argmax over the NW warp keys, publish the CTA candidate cluster-wide
-    if (wid == 0) {
+    PT(5);
+    // ---- (c) every warp: CTA argmax over the NW warp keys (same result everywhere), then the
+    // CTA's threads push the packet chunks (CTA r, chunk c) lane-parallel with st.async
+    {
       const double kv = lane < NW ? wkey_v[lane] : 0.0;
       const int kr = lane < NW ? wkey_r[lane] : 0x7fffffff;
       double cv;
       int crow, cw;
       warp_argmax_redux(kv, kr, cv, crow, cw);
-      const T mine = wrow_s[cw * KB + lane];
-      const T pj = wrow_s[cw * KB + jj];
-      const T rc = (lane == 0 && cv != 0.0) ? rcp_of(pj) : zero_of<T>();
-      const uint32_t doff = (uint32_t)(((size_t)(par * NC + rank) * KB + lane) * sizeof(T));
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        if (r < CL) {
-          if (lane < kb) st_cluster(rbase_data[r] + doff, mine);
-          if (lane == 0) {
-            st_cluster(rbase_val[r] + (uint32_t)((par * NC + rank) * sizeof(double)), cv);
-            st_cluster(rbase_row[r] + (uint32_t)((par * NC + rank) * sizeof(int)), crow);
-            st_cluster(rbase_rcp[r] + (uint32_t)((par * NC + rank) * sizeof(T)), rc);
-          }
-        }
+      const double2* src = reinterpret_cast<const double2*>(wrow_s + cw * KB);
+      const uint32_t slot = smem_u32(cand_pk + (size_t)(par * NC + rank) * PK::PKC);
+      const uint32_t bar = smem_u32(&pbar[par]);
+      for (int si = tid; si < CL * PK::PKC; si += NTHR) {
+        const int r = si / PK::PKC, c = si - r * PK::PKC;
+        double2 v;
+        if (c < PK::DC) v = src[c];
+        else if (c == PK::DC) v = make_double2(cv, __longlong_as_double((long long)crow));
+        else v = as_d2(cv != 0.0 ? rcp_of(wrow_s[cw * KB + jj]) : zero_of<T>());
+        uint32_t raddr, rbar;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(slot + 16u * c), "r"(r));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(bar), "r"(r));
+        st_async16(raddr, v.x, v.y, rbar);
       }
     }
+    if (tid == 0) mbar_expect_tx(&pbar[par], pk_tx);
     PT(1);
-    cluster.sync();
+    mbar_wait(&pbar[par], (uint32_t)((jj >> 1) & 1));
     PT(2);
     // ---- (d) winner among the CL CTA candidates (identical everywhere)
     double gv;
     int grow, gl;
     {
-      const double v = lane < NC ? cand_val[par * NC + lane] : 0.0;
-      const int rr = lane < NC ? cand_row[par * NC + lane] : 0x7fffffff;
-      warp_argmax_redux(v, rr, gv, grow, gl);
+      double2 kk = make_double2(0.0, __longlong_as_double(0x7fffffffLL));
+      if (lane < NC) kk = cand_pk[(size_t)(par * NC + lane) * PK::PKC + PK::DC];
+      warp_argmax_redux(kk.x, (int)__double_as_longlong(kk.y), gv, grow, gl);
     }
-    const int cs = gl;
     const int cr = grow;
-    const T* prow = cand_data + ((size_t)par * NC + cs) * KB;
-    const T rcp = cand_rcp[par * NC + cs];
+    const double2* wpk = cand_pk + (size_t)(par * NC + gl) * PK::PKC;
+    const T* prow = reinterpret_cast<const T*>(wpk);
+    const T rcp = from_d2<T>(wpk[PK::DC + 1]);
     const bool zero_piv = (gv == 0.0);
     if (tid == 0) pivrows[jj] = k0 + cr;
     if (tid < KB) top[jj * KB + tid] = prow[tid];
@@ -208,7 +227,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
   }
 #ifdef CPF_PANEL_TIMING
   if (rank == 0 && tid == 0)
-    for (int i = 0; i < 5; ++i) atomicAdd((unsigned long long*)&g_panel_cycles[i], (unsigned long long)tacc[i]);
+    for (int i = 0; i < 6; ++i) atomicAdd((unsigned long long*)&g_panel_cycles[i], (unsigned long long)tacc[i]);
   if (rank == 0 && tid == 0) atomicAdd((unsigned long long*)&g_panel_cycles[7], 1ull);
 #endif
 #undef PT

@@ -14,4 +14,5 @@ eng.fit_step(1)
 out = (ctypes.c_longlong * 8)()
 lib.cpf_debug_panel_cycles(out)
 n = out[7]
-print('panels', n, 'cycles per panel by phase [argmax, stage+publish, cluster.sync, winner, eliminate]:', [out[i] / max(n, 1) for i in range(5)])
+names = ['argmax', 'publish', 'cluster.sync', 'winner', 'eliminate', 'stage+syncthreads']
+print('panels', n, 'cycles per COLUMN by phase:', {names[i]: round(out[i] / max(n, 1) / 32) for i in range(6)})
