@@ -30,6 +30,7 @@ struct ApiError : std::runtime_error {
 #include "cpf_common.cuh"
 #include "lu.cuh"
 #include "lu3.cuh"
+#include "lu4.cuh"
 #include "phi.cuh"
 #include "small_ops.cuh"
 #include "tensor_pass.cuh"
@@ -89,6 +90,7 @@ struct Engine final : EngineBase {
   cudaStream_t ls = nullptr;   // stream the launch helpers target (s, or s3 for the overlapped pass B)
   cudaStream_t s3 = nullptr;   // pass B + gradient of an accepted step, overlapped with the next LU
   cudaEvent_t evF = nullptr, evG = nullptr;
+  const bool serial = [] { const char* e = getenv("CPF_SERIAL"); return e && e[0] == '1'; }();
   ncclComm_t comm = nullptr;
   int64_t nlaunch = 0;
 
@@ -289,7 +291,11 @@ struct Engine final : EngineBase {
 
   // Launch geometry for the tensor passes and the LU panel.
   int nsm_ = 148;
-  static constexpr int kLuReserveSms = 20;  // SMs left to the LU while pass B runs alongside it
+  // SMs left to the LU while pass B runs alongside it (CPF_LU_RESERVE overrides)
+  const int kLuReserveSms = [] { const char* e = getenv("CPF_LU_RESERVE"); return e ? atoi(e) : 24; }();
+  // pass B overlapped with the LU runs as a persistent grid on nsm - kLuReserveSms SMs, so the LU's
+  // small panel clusters and GEMM updates always find free SMs (CPF_PERSISTENT_B=0: plain grid)
+  const bool persistent_b = [] { const char* e = getenv("CPF_PERSISTENT_B"); return !(e && e[0] == '0'); }();
   void plan() {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -345,6 +351,10 @@ struct Engine final : EngineBase {
   }
 
   int lu3_thr = 128;  // threads per CTA of the register panel
+  // rotating-frame panel (lu4.cuh): rows/thread and threads/CTA; 0 = use k_panel_lu3
+  static constexpr int kLu4Rpt = sizeof(T) == 8 ? 2 : 1;
+  static constexpr int kLu4Thr = 256;
+  bool use_lu4 = false;
   void plan_lu3() {
     invL = dalloc<T>(2 * kLuMaxKB * kLuMaxKB);
     gring = dalloc<int>(2 * (4 * kLuMaxKB + 4));
@@ -366,6 +376,16 @@ struct Engine final : EngineBase {
       if ((nB + c[0] * c[1] - 1) / (c[0] * c[1]) <= 16) { lu3_rpt = c[0]; lu3_thr = c[1]; break; }
     }
     if (!lu3_rpt) return;  // fall back to the smem panel
+    // the rotating-frame panel wins from n_B ~ 1000 up (config 4: 1200, config 1: 4800; measured
+    // slower at 300 / 900), and its 2-3 CTA clusters co-schedule next to the persistent pass B
+    use_lu4 = nB > 1024 && (nB + kLu4Rpt * kLu4Thr - 1) / (kLu4Rpt * kLu4Thr) <= 16;
+    if (const char* e = getenv("CPF_PANEL_V3")) if (e[0] == '1') use_lu4 = false;
+    if (use_lu4) {
+      const size_t smem = panel4_smem_bytes<T>(16, kLu4Thr, kLu4Rpt);
+      CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu4<T, kLu4Rpt, kLu4Thr>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+      CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu4<T, kLu4Rpt, kLu4Thr>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
     auto setattr = [&](auto kern, int thr) {
       const size_t smem = panel3_smem_bytes<T>(16, kLuMaxKB, thr);
       CPF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -374,6 +394,24 @@ struct Engine final : EngineBase {
     setattr(k_panel_lu3<T, kLuMaxKB, 1, 128>, 128);
     if constexpr (sizeof(T) == 8) setattr(k_panel_lu3<T, kLuMaxKB, 2, 256>, 256);
     else setattr(k_panel_lu3<T, kLuMaxKB, 1, 256>, 256);
+  }
+
+  void launch_panel4(int k0, int kb, int cl, int gate_running, LuWork wk, T* invl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(kLu4Thr);
+    cfg.dynamicSmemBytes = panel4_smem_bytes<T>(cl, kLu4Thr, kLu4Rpt);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_panel_lu4<T, kLu4Rpt, kLu4Thr>, Phi, nB, nB, k0, kb, wk, invl,
+                                      (const LmDeviceState*)st, gate_running));
+    ++nlaunch;
   }
 
   template <int RPTc, int THR>
@@ -710,7 +748,7 @@ struct Engine final : EngineBase {
           launch(k_krmid<T>, nblocks(Lmid * db.WS, 256), 256, 0, F, mg, Lmid, R, db.WS, (T*)KMd, cst, cfl, gate, 1);
         dispatch_nt([&](auto ntc) {
           constexpr int NTc = decltype(ntc)::value;
-          if (ls != s && getenv("CPF_PERSISTENT_B")) {
+          if (ls != s && persistent_b) {
             // overlapped with the next LU: persistent grid that leaves SMs for the panel cluster
             const int64_t items = (int64_t)db.tiles * Cloc * db_chunks;
             const int ctas = (int)std::min<int64_t>(items, std::max(1, nsm_ - kLuReserveSms));
@@ -882,7 +920,8 @@ struct Engine final : EngineBase {
         T* invl = invL + (size_t)slot * KB * KB;
         // panel k only needs the next block of step k-1, already updated on s
         const int cl = (m + lu3_thr * lu3_rpt - 1) / (lu3_thr * lu3_rpt);
-        if (lu3_thr == 128) launch_panel3<1, 128>(k0, kb, cl, gate_running, wk, invl);
+        if (use_lu4) launch_panel4(k0, kb, (m + kLu4Rpt * kLu4Thr - 1) / (kLu4Rpt * kLu4Thr), gate_running, wk, invl);
+        else if (lu3_thr == 128) launch_panel3<1, 128>(k0, kb, cl, gate_running, wk, invl);
         else if constexpr (sizeof(T) == 8) launch_panel3<2, 256>(k0, kb, cl, gate_running, wk, invl);
         else launch_panel3<1, 256>(k0, kb, cl, gate_running, wk, invl);
         CPF_CUDA_CHECK(cudaEventRecord(evP, s));
@@ -1213,15 +1252,21 @@ struct Engine final : EngineBase {
            (const DevFlags*)fl, ga);
     // fork: pass B (M_N of the new model) + gradient on s3, while s factors the next step's
     // core system Phi(mu_{t+1}, cache_{t+1}) -- independent of Y, so the two overlap
-    CPF_CUDA_CHECK(cudaEventRecord(evF, s));
-    CPF_CUDA_CHECK(cudaStreamWaitEvent(s3, evF, 0));
-    ls = s3;
-    pass_b(A, M, ga);
-    gradient(ga);
-    ls = s;
-    CPF_CUDA_CHECK(cudaEventRecord(evG, s3));
-    prepare_core(g);
-    CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evG, 0));
+    if (serial) {  // diagnostic (CPF_SERIAL=1): no overlap, phases time standalone
+      pass_b(A, M, ga);
+      gradient(ga);
+      prepare_core(g);
+    } else {
+      CPF_CUDA_CHECK(cudaEventRecord(evF, s));
+      CPF_CUDA_CHECK(cudaStreamWaitEvent(s3, evF, 0));
+      ls = s3;
+      pass_b(A, M, ga);
+      gradient(ga);
+      ls = s;
+      CPF_CUDA_CHECK(cudaEventRecord(evG, s3));
+      prepare_core(g);
+      CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evG, 0));
+    }
     launch(k_clear_pending, 1, 1, 0, fl);
   }
 

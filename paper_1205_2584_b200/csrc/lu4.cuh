@@ -1,0 +1,291 @@
+// LU v4 panel: k_panel_lu4 -- register-resident m x 32 panel with a ROTATING register frame.
+//
+// Same algorithm and interface as k_panel_lu3 (lu3.cuh): partial pivoting by |a| (|re|+|im| for
+// complex, LAPACK's cabs1), ties to the smaller row, pivot rows retired logically and written
+// once at the end, interchange emitted as a gather list, inv(L11) for k_u12.  What changes is
+// how a thread addresses its row registers.  The 32 columns are processed in 4 chunks of 8; the
+// 8 columns of a chunk are unrolled at compile time and the thread's row is kept in a frame
+// a[0..31] whose column u is the chunk's u-th column -- so the pivot column, the next column and
+// the elimination range are all static register indices (no 32-way predicated selects per
+// column).  At the end of a chunk the 8 finished columns are flushed to shared memory and the
+// frame shifts left by 8.  Rows per CTA are large (RPT x NTHR = 640 for fp64), so the panel of a
+// 1200-row system needs a cluster of 2 CTAs instead of 10 -- small clusters also co-schedule
+// next to a running tensor pass.
+//
+// Per column: warp argmax -> CTA argmax (one __syncthreads) -> the CTA's candidate packet
+// (frame row, {|pivot|, row}, 1/pivot) is pushed into every CTA of the cluster with st.async,
+// completing tx-bytes on the receiver's mbarrier -> wait on the local mbarrier -> winner ->
+// elimination of the (static) remaining frame columns.
+#pragma once
+#include <cooperative_groups.h>
+#include "cpf_common.cuh"
+#include "lu.cuh"
+#include "lu3.cuh"
+
+namespace cpf {
+
+template <class T>
+size_t panel4_smem_bytes(int CL, int nthr, int rpt) {
+  constexpr int KB = kLuMaxKB;
+  const size_t NW = (size_t)nthr / 32;
+  const size_t pkc = (size_t)KB * sizeof(T) / 16 + 2;
+  size_t b = 16 + 16 * 2 * (size_t)CL * pkc;                     // mbarriers + packets
+  b += sizeof(T) * ((size_t)KB * nthr * rpt + NW * KB + (size_t)KB * KB);  // fin + wrow_s + top
+  b += sizeof(double) * NW + sizeof(int) * NW + sizeof(int) * 4 * KB;
+  return (b + 15) & ~(size_t)15;
+}
+
+template <class T, int RPT, int NTHR>
+__global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n, int lda, int k0, int kb, LuWork w,
+                                                       T* __restrict__ invL, const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  constexpr int KB = kLuMaxKB;  // 32
+  constexpr int CH = 8;         // columns per static chunk
+  constexpr int NW = NTHR / 32;
+  constexpr int ROWS = RPT * NTHR;  // rows per CTA
+  using PK = PanelPacket<T, KB>;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* pbar = reinterpret_cast<uint64_t*>(smem_raw);               // [2] packet arrivals (by parity)
+  double2* cand_pk = reinterpret_cast<double2*>(smem_raw + 16);         // [2][CL][PKC]
+  T* fin = reinterpret_cast<T*>(cand_pk + (size_t)2 * CL * PK::PKC);   // [KB][ROWS] finished columns
+  T* wrow_s = fin + (size_t)KB * ROWS;                                  // [NW][KB] warp candidates
+  T* top = wrow_s + (size_t)NW * KB;                                    // [KB][KB] (rank 0: L11 for inv)
+  double* wkey_v = reinterpret_cast<double*>(top + (size_t)KB * KB);    // [NW]
+  int* wkey_r = reinterpret_cast<int*>(wkey_v + NW);                    // [NW]
+  int* pivrows = wkey_r + NW;                                           // [KB]
+  int* Dl = pivrows + KB;                                               // [KB]
+  int* Vl = Dl + KB;                                                    // [KB]
+  int* misc = Vl + KB;                                                  // [KB]
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int m = n - k0;
+  T a[RPT][KB];  // frame: a[j][q] = column (c8 + q) of row j
+  bool alive[RPT];
+  int myrow[RPT];  // panel-relative row index
+  int pcol[RPT];   // pivot column of a retired row
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    myrow[j] = rank * ROWS + j * NTHR + tid;
+    alive[j] = myrow[j] < m;
+    pcol[j] = -1;
+    const T* src = A + (int64_t)(k0 + myrow[j]) + (int64_t)lda * k0;
+#pragma unroll
+    for (int q = 0; q < KB; ++q) a[j][q] = (alive[j] && q < kb) ? src[(int64_t)lda * q] : zero_of<T>();
+  }
+  if (tid == 0) {
+    mbar_init(&pbar[0], 1);
+    mbar_init(&pbar[1], 1);
+    fence_mbar_init();
+  }
+  cluster.sync();  // remote CTAs may target pbar only once it is initialised
+  const uint32_t pk_tx = (uint32_t)(CL * PK::PKC * 16);
+  const uint32_t bar0_u32 = smem_u32(&pbar[0]), bar1_u32 = smem_u32(&pbar[1]);
+
+#ifdef CPF_PANEL_TIMING
+  long long tacc[6] = {0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+#define PT(i) do { long long tn = clock64(); tacc[i] += tn - tprev; tprev = tn; } while (0)
+#else
+#define PT(i) do {} while (0)
+#endif
+
+#pragma unroll 1
+  for (int c8 = 0; c8 < kb; c8 += CH) {
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int jj = c8 + u;
+      if (jj >= kb) break;
+      const int par = u & 1;  // == jj & 1 (c8 is a multiple of 8)
+      // ---- (a) my best alive row in frame column u, then warp argmax (ties -> smaller row)
+      double bv = 0.0;
+      int bj = 0, brow = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        if (!alive[j]) continue;
+        const double v = pivmag(a[j][u]);
+        if (brow == 0x7fffffff || v > bv) { bv = v; bj = j; brow = myrow[j]; }
+      }
+      double wv;
+      int wrow, wlane;
+      warp_argmax_redux(bv, brow, wv, wrow, wlane);
+      PT(0);
+      // ---- (b) the warp's best lane stages its frame row; lane 0 posts the warp key
+      if (lane == wlane) {
+        T* dst = wrow_s + wid * KB;
+#pragma unroll
+        for (int q = 0; q < KB; ++q) {
+          T sel = a[0][q];
+#pragma unroll
+          for (int j = 1; j < RPT; ++j)
+            if (bj == j) sel = a[j][q];
+          dst[q] = sel;
+        }
+        wkey_v[wid] = wv;
+        wkey_r[wid] = wrow;
+      }
+      __syncthreads();
+      PT(5);
+      // ---- (c) every warp: CTA argmax over the NW warp keys; the CTA's threads push the packet
+      {
+        const double kv = lane < NW ? wkey_v[lane] : 0.0;
+        const int kr = lane < NW ? wkey_r[lane] : 0x7fffffff;
+        double cv;
+        int crow, cw;
+        warp_argmax_redux(kv, kr, cv, crow, cw);
+        const double2* src = reinterpret_cast<const double2*>(wrow_s + cw * KB);
+        const uint32_t slot = smem_u32(cand_pk + (size_t)(par * CL + rank) * PK::PKC);
+        for (int si = tid; si < CL * PK::PKC; si += NTHR) {
+          const int r = si / PK::PKC, c = si - r * PK::PKC;
+          double2 v;
+          if (c < PK::DC) v = src[c];
+          else if (c == PK::DC) v = make_double2(cv, __longlong_as_double((long long)crow));
+          else v = as_d2(cv != 0.0 ? rcp_of(wrow_s[cw * KB + u]) : zero_of<T>());
+          uint32_t raddr, rbar;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(slot + 16u * c), "r"(r));
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(par ? bar1_u32 : bar0_u32), "r"(r));
+          st_async16(raddr, v.x, v.y, rbar);
+        }
+      }
+      if (tid == 0) mbar_expect_tx(&pbar[par], pk_tx);
+      PT(1);
+      mbar_wait(&pbar[par], (uint32_t)((jj >> 1) & 1));
+      PT(2);
+      // ---- (d) winner among the CL CTA candidates (identical everywhere)
+      double gv;
+      int cr, gl;
+      {
+        double2 kk = make_double2(0.0, __longlong_as_double(0x7fffffffLL));
+        if (lane < CL) kk = cand_pk[(size_t)(par * CL + lane) * PK::PKC + PK::DC];
+        warp_argmax_redux(kk.x, (int)__double_as_longlong(kk.y), gv, cr, gl);
+      }
+      const double2* wpk = cand_pk + (size_t)(par * CL + gl) * PK::PKC;
+      const T rcp = from_d2<T>(wpk[PK::DC + 1]);
+      const bool zero_piv = (gv == 0.0);
+      if (tid == 0) pivrows[jj] = k0 + cr;
+      if (zero_piv && rank == 0 && tid == 0 && *w.info == 0) *w.info = k0 + jj + 1;
+      PT(3);
+      // ---- (e) elimination of the frame columns u+1 .. KB-1 (static range)
+      T l[RPT];
+      bool el[RPT];
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        if (alive[j] && myrow[j] == cr) { alive[j] = false; pcol[j] = jj; }
+        el[j] = alive[j] && !zero_piv;
+        l[j] = el[j] ? mul(a[j][u], rcp) : zero_of<T>();
+      }
+      if constexpr (sizeof(T) == 8) {
+#pragma unroll
+        for (int c = (u + 1) / 2; c < KB / 2; ++c) {
+          const double2 v = wpk[c];
+#pragma unroll
+          for (int j = 0; j < RPT; ++j) {
+            if (2 * c > u) fms_acc(a[j][2 * c], l[j], from_d2<T>(make_double2(v.x, 0.0)));
+            fms_acc(a[j][2 * c + 1], l[j], from_d2<T>(make_double2(v.y, 0.0)));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = u + 1; c < KB; ++c) {
+          const T v = from_d2<T>(wpk[c]);
+#pragma unroll
+          for (int j = 0; j < RPT; ++j) fms_acc(a[j][c], l[j], v);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < RPT; ++j)
+        if (el[j]) a[j][u] = l[j];  // L multiplier; the pivot row keeps its U entry
+      PT(4);
+    }
+    // ---- chunk end: flush the 8 finished frame columns, shift the frame left by 8
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+#pragma unroll
+      for (int q = 0; q < CH; ++q) fin[(size_t)(c8 + q) * ROWS + j * NTHR + tid] = a[j][q];
+#pragma unroll
+      for (int q = 0; q < KB - CH; ++q) a[j][q] = a[j][q + CH];
+#pragma unroll
+      for (int q = KB - CH; q < KB; ++q) a[j][q] = zero_of<T>();
+    }
+  }
+#ifdef CPF_PANEL_TIMING
+  if (rank == 0 && tid == 0)
+    for (int i = 0; i < 6; ++i) atomicAdd((unsigned long long*)&g_panel_cycles[i], (unsigned long long)tacc[i]);
+  if (rank == 0 && tid == 0) atomicAdd((unsigned long long*)&g_panel_cycles[7], 1ull);
+#endif
+#undef PT
+  __syncthreads();
+  // ---- interchange bookkeeping (same rule as k_panel_lu): D (non-pivot top rows, ascending)
+  // -> V (pivot rows from below, pick order)
+  if (wid == 0) {
+    const bool live = lane < kb;
+    const int toprow = k0 + lane;
+    bool top_is_piv = false;
+    for (int q = 0; q < kb; ++q) top_is_piv |= (pivrows[q] == toprow);
+    const unsigned dmask = __ballot_sync(0xffffffffu, live && !top_is_piv);
+    const unsigned vmask = __ballot_sync(0xffffffffu, live && pivrows[live ? lane : 0] >= k0 + kb);
+    if (live && !top_is_piv) Dl[__popc(dmask & ((1u << lane) - 1u))] = toprow;
+    if (live && pivrows[lane] >= k0 + kb) Vl[__popc(vmask & ((1u << lane) - 1u))] = pivrows[lane];
+    if (lane == 0) misc[0] = __popc(dmask);
+  }
+  __syncthreads();
+  const int nd = misc[0];
+  // every row to its final position: pivot rows to k0 + pivot column, displaced top rows to
+  // V[d], the rest stay
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    if (myrow[j] >= m) continue;
+    const int o = k0 + myrow[j];
+    int pos = o;
+    if (pcol[j] >= 0) {
+      pos = k0 + pcol[j];
+    } else if (o < k0 + kb) {
+      for (int d = 0; d < nd; ++d)
+        if (Dl[d] == o) pos = Vl[d];
+    }
+    T* dst = A + (int64_t)pos + (int64_t)lda * k0;
+    for (int q = 0; q < kb; ++q) dst[(int64_t)lda * q] = fin[(size_t)q * ROWS + j * NTHR + tid];
+  }
+  cluster.sync();  // every CTA's rows are in place (global writes ordered at cluster scope)
+  if (rank == 0) {
+    for (int e = tid; e < KB * KB; e += NTHR) {
+      const int r = e / KB, q = e % KB;
+      top[e] = (r < kb && q < kb) ? A[(int64_t)(k0 + r) + (int64_t)lda * (k0 + q)] : zero_of<T>();
+    }
+    __syncthreads();
+    // inv(L11): lane c solves L x = e_c (unit lower)
+    if (wid == 0 && invL) {
+      const int c = lane;
+      T x[KB];
+#pragma unroll
+      for (int i = 0; i < KB; ++i) {
+        T v = from_real<T>((i == c) ? 1.0 : 0.0);
+#pragma unroll
+        for (int j = 0; j < i; ++j) fms_acc(v, top[i * KB + j], x[j]);
+        x[i] = (i < c) ? zero_of<T>() : v;
+      }
+      if (c < kb)
+#pragma unroll
+        for (int i = 0; i < KB; ++i)
+          if (i < kb) invL[i + KB * c] = x[i];
+    }
+    if (wid == 1) {
+      int g = 0;
+      for (int q = 0; q < kb; ++q) {
+        if (pivrows[q] != k0 + q) {
+          if (lane == 0) { w.gather[2 * g] = k0 + q; w.gather[2 * g + 1] = pivrows[q]; }
+          ++g;
+        }
+      }
+      for (int d = 0; d < nd; ++d) {
+        if (lane == 0) { w.gather[2 * g] = Vl[d]; w.gather[2 * g + 1] = Dl[d]; }
+        ++g;
+      }
+      if (lane == 0) *w.gcount = g;
+    }
+  }
+}
+
+}  // namespace cpf
