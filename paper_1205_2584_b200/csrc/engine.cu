@@ -31,6 +31,7 @@ struct ApiError : std::runtime_error {
 #include "lu.cuh"
 #include "lu3.cuh"
 #include "lu4.cuh"
+#include "tri_inv.cuh"
 #include "phi.cuh"
 #include "small_ops.cuh"
 #include "tensor_pass.cuh"
@@ -105,6 +106,9 @@ struct Engine final : EngineBase {
   T *Cg = nullptr, *Ccg = nullptr, *Gx = nullptr, *Gp = nullptr, *Gf = nullptr, *Gti = nullptr, *Gi = nullptr;
   T *W1 = nullptr, *Sm = nullptr;
   T *wvec = nullptr, *fvec = nullptr, *xvec = nullptr, *Phi = nullptr;
+  // explicit (factored) inverse of Phi: B w = inv(U) inv(L) P w as two triangular mat-vecs
+  T *PhiInv = nullptr, *TriTmp = nullptr, *yvec = nullptr, *tmv_part = nullptr;
+  bool use_inv = false;
   T *A1c = nullptr, *KMc = nullptr, *WNc = nullptr, *zpart = nullptr, *m1part = nullptr, *bpart = nullptr;
   T *A1r = nullptr, *KMr = nullptr, *WNr = nullptr;  // non-conj operands of the direct residual
   T *pa_out = nullptr, *pb_out = nullptr, *pb_all = nullptr;
@@ -236,7 +240,7 @@ struct Engine final : EngineBase {
     for (auto& e : evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     void* ptrs[] = {Yown, A, Ac, M, Mc, D, G, Cand, V1, V2, V3, V4, Cg, Ccg, Gx, Gp, Gf, Gti, Gi, W1, Sm,
                     wvec, fvec, xvec, Phi, A1c, KMc, WNc, A1r, KMr, WNr, zpart, m1part, bpart, pa_out, pb_out, pb_all,
-                    norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL, WNd, KMd, gring};
+                    norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL, WNd, KMd, gring, PhiInv, TriTmp, yvec, tmv_part};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (hst) cudaFreeHost(hst);
@@ -261,6 +265,16 @@ struct Engine final : EngineBase {
     Gf = dalloc<T>(R2); Gti = dalloc<T>(N * R2); Gi = dalloc<T>(N * R2); W1 = dalloc<T>(N * R2); Sm = dalloc<T>(N * R2);
     wvec = dalloc<T>(nB); fvec = dalloc<T>(nB); xvec = dalloc<T>(nB);
     Phi = dalloc<T>((size_t)nB * nB);
+    // explicit inverse pays off while its ~(4/3) n^3 flops stay below the latency of six
+    // substitutions (measured: n = 1200 yes, n = 4800 no); CPF_NO_INV=1 disables
+    use_inv = nB <= 2560;
+    if (const char* e = getenv("CPF_NO_INV")) if (e[0] == '1') use_inv = false;
+    if (use_inv) {
+      PhiInv = dalloc<T>((size_t)nB * nB);
+      TriTmp = dalloc<T>((size_t)nB * nB);
+      yvec = dalloc<T>(nB);
+      tmv_part = dalloc<T>((size_t)((nB + kTmvCols - 1) / kTmvCols) * nB);
+    }
     A1c = dalloc<T>((size_t)I1 * RP + 2);
     KMc = dalloc<T>((size_t)Lmid * RP + 2);
     WNc = dalloc<T>((size_t)std::max<int64_t>(Cloc, 1) * RP + 2);
@@ -984,10 +998,42 @@ struct Engine final : EngineBase {
     ph_end();
   }
   // f = B w  (flm-b: Phi^{-1} w; flm-a: K Phi^{-1} w)
+  // inv(L), inv(U) of the factored Phi (tri_inv.cuh), packed like the factors
+  void tri_invert(int gate_running) {
+    ph_begin(kPhLU);
+    const int nblk = (nB + 31) / 32;
+    launch(k_tri_inv_diag<T>, nblk, 64, 0, (const T*)Phi, nB, PhiInv, (const LmDeviceState*)st, gate_running);
+    for (int sz = 32; sz < nB; sz *= 2) {
+      const int npairs = (nB + 2 * sz - 1) / (2 * sz);
+      const dim3 grid((sz + 63) / 64, (sz + 63) / 64, 2 * npairs);
+      launch(k_tri_level<T, 0>, grid, 256, 0, (const T*)Phi, PhiInv, TriTmp, nB, sz, (const LmDeviceState*)st,
+             gate_running);
+      launch(k_tri_level<T, 1>, grid, 256, 0, (const T*)Phi, PhiInv, TriTmp, nB, sz, (const LmDeviceState*)st,
+             gate_running);
+    }
+    ph_end();
+  }
+
   void apply_b(const T* w, T* f, int gate_running) {
     ph_begin(kPhSolve);
     launch(k_perm_gather<T>, nblocks(nB, 256), 256, 0, w, (const int*)lu.perm, nB, xvec, (const LmDeviceState*)st,
            gate_running);
+    if (use_inv) {
+      const dim3 grid((nB + kTmvRows - 1) / kTmvRows, (nB + kTmvCols - 1) / kTmvCols);
+      const int nsl = (int)grid.y;
+      launch(k_tri_mv<T, true>, grid, 256, 0, (const T*)PhiInv, nB, (const T*)xvec, tmv_part, (const LmDeviceState*)st,
+             gate_running);
+      launch(k_tri_mv_sum<T, true>, nblocks(nB, 256), 256, 0, (const T*)tmv_part, nsl, nB, (const T*)xvec, yvec,
+             (const LmDeviceState*)st, gate_running);
+      launch(k_tri_mv<T, false>, grid, 256, 0, (const T*)PhiInv, nB, (const T*)yvec, tmv_part, (const LmDeviceState*)st,
+             gate_running);
+      launch(k_tri_mv_sum<T, false>, nblocks(nB, 256), 256, 0, (const T*)tmv_part, nsl, nB, (const T*)yvec, xvec,
+             (const LmDeviceState*)st, gate_running);
+      launch(k_apply_k<T>, nblocks(nB, 256), 256, 0, (const T*)xvec, N, R, (const T*)Gp, f, (const LmDeviceState*)st,
+             gate_running);
+      ph_end();
+      return;
+    }
     const int nblk = (nB + 31) / 32;
     // ready flags are cleared in-stream (graph-replay safe: no host-side epoch)
     CPF_CUDA_CHECK(cudaMemsetAsync(lu.ticket, 0, sizeof(int) * 2, s));
@@ -1011,6 +1057,7 @@ struct Engine final : EngineBase {
     launch(k_phi_assemble<T>, nblocks((int64_t)nB * nB, 256), 256, 0, Phi, N, R, (const T*)Cg, (const T*)Gi,
            (const T*)Gp, (const T*)Gf, (const LmDeviceState*)st, gr);
     lu_factor(gr);
+    if (use_inv) tri_invert(gr);
   }
 
   void candidate(int refine_steps, int gate, bool core_ready = false) {

@@ -1,0 +1,226 @@
+// Explicit inverse of the core system's LU factors, so that the three B-applications of a step
+// (candidate + two refinement rounds) are triangular matrix-VECTOR products instead of
+// latency-bound substitutions.  The reference itself applies an explicit inverse:
+// B = np.linalg.inv(K^-1 + Psi) (hessian.py:196-211, LAPACK getri); here the inverse is kept
+// factored, B w = inv(U) inv(L) P w.
+//
+// Storage: Inv (n x n, column-major) holds inv(L) strictly below the diagonal (unit diagonal
+// implicit) and inv(U) on and above it -- the same packing as the LU factors.
+// Algorithm (recursive doubling, every level one batched launch per product):
+//   level 0: invert every 32x32 diagonal block (one CTA each);
+//   level s: for adjacent blocks (b1, b2) of size s
+//     L: inv([L11 0; L21 L22])  -> X21 = -inv(L22) (L21 inv(L11))
+//     U: inv([U11 U12; 0 U22])  -> X12 = -inv(U11) (U12 inv(U22))
+// Products are fp64/complex128 DFMA tiles (64x64 per CTA, 16 K-rows per smem stage).
+#pragma once
+#include "cpf_common.cuh"
+
+namespace cpf {
+
+template <class T>
+__global__ void __launch_bounds__(64) k_tri_inv_diag(const T* __restrict__ LU, int n, T* __restrict__ Inv,
+                                                     const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  __shared__ T blk[32][33];
+  const int b0 = blockIdx.x * 32;
+  const int bs = min(32, n - b0);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < 32 * 32; e += 64) {
+    const int i = e % 32, j = e / 32;
+    blk[i][j] = (i < bs && j < bs) ? LU[(int64_t)(b0 + i) + (int64_t)n * (b0 + j)] : zero_of<T>();
+  }
+  __syncthreads();
+  const int c = lane;
+  if (c >= bs) return;
+  T x[32];
+  if (wid == 0) {
+    // unit lower: x = inv(L) e_c, rows i > c
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      T v = from_real<T>(i == c ? 1.0 : 0.0);
+#pragma unroll
+      for (int j = 0; j < i; ++j) fms_acc(v, blk[i][j], x[j]);
+      x[i] = i < c ? zero_of<T>() : v;
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i > c && i < bs) Inv[(int64_t)(b0 + i) + (int64_t)n * (b0 + c)] = x[i];
+  } else {
+    // upper: x = inv(U) e_c, rows i <= c
+#pragma unroll
+    for (int i = 31; i >= 0; --i) {
+      T v = from_real<T>(i == c ? 1.0 : 0.0);
+#pragma unroll
+      for (int j = i + 1; j < 32; ++j) fms_acc(v, blk[i][j], x[j]);
+      x[i] = (i > c || i >= bs) ? zero_of<T>() : mul(v, rcp_of(blk[i][i]));
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i <= c) Inv[(int64_t)(b0 + i) + (int64_t)n * (b0 + c)] = x[i];
+  }
+}
+
+// Operand kinds of the level products
+enum TriOp { kOpFull = 0, kOpInvL = 1, kOpInvU = 2 };
+
+template <class T>
+__device__ __forceinline__ T tri_elem(const T* M, int n, int r, int c, int kind) {
+  if (kind == kOpInvL) {
+    if (r == c) return from_real<T>(1.0);
+    if (r < c) return zero_of<T>();
+  } else if (kind == kOpInvU) {
+    if (r > c) return zero_of<T>();
+  }
+  return M[(int64_t)r + (int64_t)n * c];
+}
+
+// One level product for every (pair, triangle): C = alpha * opA(A) * opB(B), all blocks inside
+// n x n column-major matrices.  blockIdx.z = 2 * pair + tri (tri 0: L, 1: U).
+//   step 0 (T):  L: T[b2,b1] = L21 * inv(L11)      U: T[b1,b2] = U12 * inv(U22)
+//   step 1 (X):  L: X[b2,b1] = -inv(L22) * T        U: X[b1,b2] = -inv(U11) * T
+template <class T, int STEP>
+__global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* __restrict__ Inv, T* __restrict__ Tmp,
+                                                   int n, int s, const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  const int pair = blockIdx.z >> 1, tri = blockIdx.z & 1;
+  const int b1 = 2 * pair * s, b2 = b1 + s;
+  if (b2 >= n) return;
+  const int s1 = s, s2 = min(s, n - b2);
+  // output block: rows/cols and operands
+  int m, nn, kk, ra, ca, rb, cb, rc, cc, kindA, kindB;
+  const T *Am, *Bm;
+  T* Cm;
+  double alpha;
+  if (tri == 0) {  // L
+    m = s2; nn = s1;
+    if (STEP == 0) { kk = s1; Am = LU; ra = b2; ca = b1; kindA = kOpFull; Bm = Inv; rb = b1; cb = b1; kindB = kOpInvL; alpha = 1.0; Cm = Tmp; }
+    else { kk = s2; Am = Inv; ra = b2; ca = b2; kindA = kOpInvL; Bm = Tmp; rb = b2; cb = b1; kindB = kOpFull; alpha = -1.0; Cm = Inv; }
+    rc = b2; cc = b1;
+  } else {  // U
+    m = s1; nn = s2;
+    if (STEP == 0) { kk = s2; Am = LU; ra = b1; ca = b2; kindA = kOpFull; Bm = Inv; rb = b2; cb = b2; kindB = kOpInvU; alpha = 1.0; Cm = Tmp; }
+    else { kk = s1; Am = Inv; ra = b1; ca = b1; kindA = kOpInvU; Bm = Tmp; rb = b1; cb = b2; kindB = kOpFull; alpha = -1.0; Cm = Inv; }
+    rc = b1; cc = b2;
+  }
+  const int tm = blockIdx.x * 64, tn = blockIdx.y * 64;
+  if (tm >= m || tn >= nn) return;
+  constexpr int KS = 16 * 8 / (int)sizeof(T);  // K rows per stage (8 for complex: 48 KB static smem)
+  // triangular operands: skip the K range that only multiplies zeros
+  int kbeg = 0, kend = kk;
+  if (kindA == kOpInvL) kend = min(kend, tm + 64);  // row i needs k <= i
+  if (kindA == kOpInvU) kbeg = tm;                   // row i needs k >= i
+  if (kindB == kOpInvL) kbeg = max(kbeg, tn);        // col j needs k >= j
+  if (kindB == kOpInvU) kend = min(kend, tn + 64);   // col j needs k <= j
+  kbeg &= ~(KS - 1);
+  __shared__ T As[2][KS][64 + 1];
+  __shared__ T Bs[2][KS][64 + 1];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;  // 16 x 16 threads, 4 x 4 outputs each
+  T acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = zero_of<T>();
+  // register-staged prefetch of the next K slab (KS x 64 of A and B: 4 + 4 elements per thread)
+  constexpr int PER = 64 * KS / 256;
+  T pa[PER], pb[PER];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int e = tid + 256 * t;
+      const int i = e % 64, q = e / 64;
+      pa[t] = (tm + i < m && k0 + q < kend) ? tri_elem(Am, n, ra + tm + i, ca + k0 + q, kindA) : zero_of<T>();
+      const int q2 = e % KS, j = e / KS;
+      pb[t] = (k0 + q2 < kend && tn + j < nn) ? tri_elem(Bm, n, rb + k0 + q2, cb + tn + j, kindB) : zero_of<T>();
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int e = tid + 256 * t;
+      As[buf][e / 64][e % 64] = pa[t];
+      Bs[buf][e % KS][e / KS] = pb[t];
+    }
+  };
+  int buf = 0;
+  if (kbeg < kend) {
+    fetch(kbeg);
+    stash(0);
+  }
+  __syncthreads();
+  for (int k0 = kbeg; k0 < kend; k0 += KS) {
+    const bool more = k0 + KS < kend;
+    if (more) fetch(k0 + KS);
+#pragma unroll
+    for (int q = 0; q < KS; ++q) {
+      T av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[buf][q][tx + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[buf][q][ty + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fma_acc(acc[i][j], av[i], bv[j]);
+    }
+    if (more) stash(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = tm + tx + 16 * i, c = tn + ty + 16 * j;
+      if (r < m && c < nn) Cm[(int64_t)(rc + r) + (int64_t)n * (cc + c)] = scale(acc[i][j], alpha);
+    }
+}
+
+// y = op(Inv) x for the packed triangular inverse: LOWER -> unit-lower inv(L), else inv(U).
+// Two launches: k_tri_mv partial products over (64-row tile) x (128-column slice) CTAs, then
+// k_tri_mv_sum adds the slices (fixed order: deterministic).  Part: [nslices][n].
+constexpr int kTmvRows = 64, kTmvCols = 128;
+template <class T, bool LOWER>
+__global__ void __launch_bounds__(256) k_tri_mv(const T* __restrict__ Inv, int n, const T* __restrict__ x,
+                                                T* __restrict__ part, const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  __shared__ T red[4][kTmvRows];
+  const int r0 = blockIdx.x * kTmvRows, c0 = blockIdx.y * kTmvCols;
+  const int tid = threadIdx.x, rl = tid % kTmvRows, g = tid / kTmvRows;
+  const int row = r0 + rl;
+  T acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = zero_of<T>();
+  const bool tile_live = LOWER ? (c0 < r0 + kTmvRows) : (c0 + kTmvCols > r0);
+  if (tile_live && row < n) {
+    const int cb = c0 + g * (kTmvCols / 4);
+#pragma unroll
+    for (int c4 = 0; c4 < kTmvCols / 4; c4 += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = cb + c4 + u;
+        const bool in = c < n && (LOWER ? c < row : c >= row);
+        if (in) fma_acc(acc[u], Inv[(int64_t)row + (int64_t)n * c], x[c]);
+      }
+    }
+  }
+  T v = acc[0];
+#pragma unroll
+  for (int u = 1; u < 8; ++u) v = add(v, acc[u]);
+  red[g][rl] = v;
+  __syncthreads();
+  if (g == 0 && row < n) part[(int64_t)blockIdx.y * n + row] = add(add(red[0][rl], red[1][rl]), add(red[2][rl], red[3][rl]));
+}
+
+template <class T, bool LOWER>
+__global__ void k_tri_mv_sum(const T* __restrict__ part, int nslices, int n, const T* __restrict__ x, T* __restrict__ y,
+                             const LmDeviceState* st, int gate_running) {
+  if (st && gate_running && (st->stopped || st->err_code)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T v = LOWER ? x[i] : zero_of<T>();
+  for (int q = 0; q < nslices; ++q) v = add(v, part[(int64_t)q * n + i]);
+  y[i] = v;
+}
+
+}  // namespace cpf
