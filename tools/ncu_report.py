@@ -7,14 +7,30 @@ KEYS = [
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "lts__t_sector_hit_rate.pct",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "launch__cluster_dim_x",
 ]
 
 
 def main(path, out=None):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    lines = [f"# {path}", f"kernel: {vals[hdr.index('Kernel Name')]}"]
+    hdr, units = rows[0], rows[1]
+    lines = [f"# {path}"]
+    seen = set()
+    for vals in rows[2:]:
+        name = vals[hdr.index('Kernel Name')]
+        if name in seen:  # one block per distinct kernel (first launch)
+            continue
+        seen.add(name)
+        lines += kernel_block(hdr, units, vals)
+    text = "\n".join(lines) + "\n"
+    if out:
+        open(out, "w").write(text)
+    print(text)
+
+
+def kernel_block(hdr, units, vals):
+    lines = ["", f"kernel: {vals[hdr.index('Kernel Name')]}"]
     for k in KEYS:
         if k in hdr:
             i = hdr.index(k)
@@ -28,10 +44,7 @@ def main(path, out=None):
                 pass
     tot = sum(v for v, _ in stalls) or 1.0
     lines.append("top stall reasons (pc sampling): " + ", ".join(f"{n} {v / tot:.0%}" for v, n in sorted(stalls, reverse=True)[:6]))
-    text = "\n".join(lines) + "\n"
-    if out:
-        open(out, "w").write(text)
-    print(text)
+    return lines
 
 
 if __name__ == "__main__":
