@@ -148,6 +148,7 @@ struct Engine final : EngineBase {
   int* gring = nullptr; // 2 gather lists + counts
   cudaStream_t s2 = nullptr;
   cudaEvent_t evP = nullptr, evB = nullptr, evJ = nullptr;
+  cudaEvent_t evB2[2] = {nullptr, nullptr};
   size_t lu_smem = 0;
 
   // CUDA graph of one iteration (replayed; all control is device-side)
@@ -232,6 +233,7 @@ struct Engine final : EngineBase {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (evP) cudaEventDestroy(evP);
     if (evB) cudaEventDestroy(evB);
+    for (auto e : evB2) if (e) cudaEventDestroy(e);
     if (evJ) cudaEventDestroy(evJ);
     if (s2) cudaStreamDestroy(s2);
     if (evF) cudaEventDestroy(evF);
@@ -310,10 +312,15 @@ struct Engine final : EngineBase {
   // pass B overlapped with the LU runs as a persistent grid on nsm - kLuReserveSms SMs, so the LU's
   // small panel clusters and GEMM updates always find free SMs (CPF_PERSISTENT_B=0: plain grid)
   const bool persistent_b = [] { const char* e = getenv("CPF_PERSISTENT_B"); return !(e && e[0] == '0'); }();
+  // next-block update fused into the panel load (PanelPrev, lu3.cuh): removes the gather / U12 /
+  // GEMM launches between consecutive panels.  Measured (1 x B200): C1 43.3 -> 51.1 it/s, C2 359 ->
+  // 405, C4 131.4 -> 131.4 (there the LU is hidden behind pass B).  CPF_LU_FUSE=0: unfused.
+  bool lu_fuse = true;
   void plan() {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     nsm_ = nsm;
+    if (const char* e = getenv("CPF_LU_FUSE")) lu_fuse = e[0] == '1';
     const size_t es = sizeof(T);
     // pass A: threads sized so 2*threads*RP*es (+W stage) fits ~160 KB
     pa_threads = 256;
@@ -380,6 +387,7 @@ struct Engine final : EngineBase {
     CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evP, cudaEventDisableTiming));
     CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
     CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evJ, cudaEventDisableTiming));
+    for (auto& e : evB2) CPF_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     lu3_rpt = 0;
     // (rows/thread, threads/CTA) candidates, smallest per-SM work first; cluster <= 16 CTAs
     const int cand[2][2] = {{1, 128}, {sizeof(T) == 8 ? 2 : 1, 256}};
@@ -410,7 +418,7 @@ struct Engine final : EngineBase {
     else setattr(k_panel_lu3<T, kLuMaxKB, 1, 256>, 256);
   }
 
-  void launch_panel4(int k0, int kb, int cl, int gate_running, LuWork wk, T* invl) {
+  void launch_panel4(int k0, int kb, int cl, int gate_running, LuWork wk, T* invl, PanelPrev<T> pv) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cl);
     cfg.blockDim = dim3(kLu4Thr);
@@ -424,12 +432,12 @@ struct Engine final : EngineBase {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_panel_lu4<T, kLu4Rpt, kLu4Thr>, Phi, nB, nB, k0, kb, wk, invl,
-                                      (const LmDeviceState*)st, gate_running));
+                                      (const LmDeviceState*)st, gate_running, pv));
     ++nlaunch;
   }
 
   template <int RPTc, int THR>
-  void launch_panel3(int k0, int kb, int cl, int gate_running, LuWork wk, T* invl) {
+  void launch_panel3(int k0, int kb, int cl, int gate_running, LuWork wk, T* invl, PanelPrev<T> pv) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cl);
     cfg.blockDim = dim3(THR);
@@ -443,7 +451,7 @@ struct Engine final : EngineBase {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_panel_lu3<T, kLuMaxKB, RPTc, THR>, Phi, nB, nB, k0, kb, wk, invl,
-                                      (const LmDeviceState*)st, gate_running));
+                                      (const LmDeviceState*)st, gate_running, pv));
     ++nlaunch;
   }
 
@@ -918,9 +926,13 @@ struct Engine final : EngineBase {
     ph_begin(kPhLU);
     launch(k_lu_init, nblocks(nB, 256), 256, 0, lu.perm, nB, lu.info);
     if (lu3_rpt) {
-      // Look-ahead right-looking LU: stream s factors panel k and updates only the next block
-      // (the columns panel k+1 needs); stream s2 applies panel k to everything else concurrently
-      // with panel k+1.  Gather lists and inv(L11) are double-buffered across steps.
+      // Look-ahead right-looking LU.  Panel k+1's columns are the "next block" of step k: the
+      // panel kernel itself applies step k's interchange and update to them while loading
+      // (PanelPrev, lu3.cuh), so consecutive panels follow each other on stream s with no
+      // kernels in between.  Stream s2 applies panel k to everything else (left columns' swaps,
+      // perm, columns >= k0 + 2 KB) concurrently with panel k+1.  Gather lists and inv(L11) are
+      // double-buffered across steps; panel k waits for s2's step k-2 (which updated its block
+      // and last read the slot panel k overwrites).
       const int KB = kLuMaxKB;
       const int np = (nB + KB - 1) / KB;
       CPF_CUDA_CHECK(cudaEventRecord(evJ, s));
@@ -932,24 +944,34 @@ struct Engine final : EngineBase {
         wk.gather = gring + slot * (4 * KB + 4);
         wk.gcount = wk.gather + 4 * KB;
         T* invl = invL + (size_t)slot * KB * KB;
-        // panel k only needs the next block of step k-1, already updated on s
+        PanelPrev<T> pv{-1, 0, nullptr, nullptr, nullptr};
+        if (k > 0 && lu_fuse) {
+          const int ps = slot ^ 1;
+          pv.kp0 = k0 - KB;
+          pv.kbp = KB;
+          pv.gather = gring + ps * (4 * KB + 4);
+          pv.gcount = pv.gather + 4 * KB;
+          pv.invL = invL + (size_t)ps * KB * KB;
+        }
+        if (k >= 2 && lu_fuse) CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evB2[slot], 0));
         const int cl = (m + lu3_thr * lu3_rpt - 1) / (lu3_thr * lu3_rpt);
-        if (use_lu4) launch_panel4(k0, kb, (m + kLu4Rpt * kLu4Thr - 1) / (kLu4Rpt * kLu4Thr), gate_running, wk, invl);
-        else if (lu3_thr == 128) launch_panel3<1, 128>(k0, kb, cl, gate_running, wk, invl);
-        else if constexpr (sizeof(T) == 8) launch_panel3<2, 256>(k0, kb, cl, gate_running, wk, invl);
-        else launch_panel3<1, 256>(k0, kb, cl, gate_running, wk, invl);
+        if (use_lu4) launch_panel4(k0, kb, (m + kLu4Rpt * kLu4Thr - 1) / (kLu4Rpt * kLu4Thr), gate_running, wk, invl, pv);
+        else if (lu3_thr == 128) launch_panel3<1, 128>(k0, kb, cl, gate_running, wk, invl, pv);
+        else if constexpr (sizeof(T) == 8) launch_panel3<2, 256>(k0, kb, cl, gate_running, wk, invl, pv);
+        else launch_panel3<1, 256>(k0, kb, cl, gate_running, wk, invl, pv);
         CPF_CUDA_CHECK(cudaEventRecord(evP, s));
-        // the next block lies in step k-1's "rest": wait for s2 to finish step k-1 (this also frees
-        // the gather/inv(L11) slot panel k+1 will write)
-        if (k > 0) CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evB, 0));
         const int nb0 = k0 + kb, nb1 = std::min(nB, k0 + 2 * kb);
-        // s: next block only
-        lu_gather(slot, nb0, nb1, 0, 0, 0, s, gate_running);
-        lu_update_cols(k0, kb, nb0, nb1, invl, s, gate_running);
+        if (!lu_fuse) {
+          // unfused: the next block's interchange + update as kernels on s, after s2's step k-1
+          if (k > 0) CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evB, 0));
+          lu_gather(slot, nb0, nb1, 0, 0, 0, s, gate_running);
+          lu_update_cols(k0, kb, nb0, nb1, invl, s, gate_running);
+        }
         // s2: left columns + the rest + perm, after panel k
         CPF_CUDA_CHECK(cudaStreamWaitEvent(s2, evP, 0));
         lu_gather(slot, 0, k0, nb1, nB, 1, s2, gate_running);
         lu_update_cols(k0, kb, nb1, nB, invl, s2, gate_running);
+        CPF_CUDA_CHECK(cudaEventRecord(evB2[slot], s2));
         CPF_CUDA_CHECK(cudaEventRecord(evB, s2));
       }
       CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evB, 0));

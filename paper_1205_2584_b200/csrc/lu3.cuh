@@ -72,9 +72,133 @@ __device__ __forceinline__ void warp_argmax_redux(double v, int row, double& wv,
   wv = __hiloint2double((int)m1, (int)m2);
 }
 
+// The previous panel's update of this panel's block, fused into the panel load.  With look-ahead,
+// panel k+1's 32 columns are exactly the "next block" of step k; instead of a row gather, U12 and a
+// GEMM launched between the two panels, panel k+1 reads its rows through step k's interchange
+// (gather list of (pos, src) pairs), forms U12 = inv(L11_k) A12 of the step's kbp top rows, and
+// applies A22 -= L21_k U12 to its own rows while they go into registers.  Rank 0 writes U12 back
+// after the kernel's first cluster barrier (panel_prev_store), when every CTA of the cluster is
+// past its loads.  The scratch aliases smem the panel uses only later (no extra footprint, so the
+// panel CTAs co-schedule with the trailing-update kernels exactly as before).
+template <class T>
+struct PanelPrev {
+  int kp0;             // previous panel's first row/column; < 0: no previous step (plain load)
+  int kbp;             // its width
+  const int* gather;   // its (pos, src) pairs
+  const int* gcount;
+  const T* invL;       // its inv(L11), KB x KB column-major
+};
+
+template <class T, int RPT, int NTHR>
+__device__ __forceinline__ void panel_load(T (&a)[RPT][kLuMaxKB], const T* __restrict__ A, int lda, int k0, int kb,
+                                           const int (&myrow)[RPT], const bool (&alive)[RPT], const PanelPrev<T>& pv,
+                                           int* gl, T* u12, T* stage = nullptr) {
+  constexpr int KB = kLuMaxKB;
+  const int tid = threadIdx.x;
+  if (pv.kp0 < 0) {
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const T* src = A + (int64_t)(k0 + myrow[j]) + (int64_t)lda * k0;
+#pragma unroll
+      for (int q = 0; q < KB; ++q) a[j][q] = (alive[j] && q < kb) ? src[(int64_t)lda * q] : zero_of<T>();
+    }
+    return;
+  }
+  const int G = *pv.gcount;
+  for (int e = tid; e < 2 * G; e += NTHR) gl[e] = pv.gather[e];
+  __syncthreads();
+  auto src_of = [&](int r) {
+    int s = r;
+    for (int g = 0; g < G; ++g)
+      if (gl[2 * g] == r) s = gl[2 * g + 1];
+    return s;
+  };
+  // A12 (the step's top rows of this block, interchanged) -> u12[i][q]
+  for (int e = tid; e < KB * KB; e += NTHR) {
+    const int i = e % KB, q = e / KB;
+    T v = zero_of<T>();
+    if (i < pv.kbp && q < kb) v = A[(int64_t)src_of(pv.kp0 + i) + (int64_t)lda * (k0 + q)];
+    u12[i * KB + q] = v;
+  }
+  __syncthreads();
+  // U12 = inv(L11) A12 (same summation order as k_u12)
+  T uv[(KB * KB + NTHR - 1) / NTHR];
+#pragma unroll
+  for (int t = 0; t < (KB * KB + NTHR - 1) / NTHR; ++t) {
+    const int e = tid + t * NTHR;
+    T acc = zero_of<T>();
+    if (e < KB * KB) {
+      const int i = e / KB, q = e % KB;
+      for (int p = 0; p <= i; ++p) fma_acc(acc, pv.invL[i + KB * p], u12[p * KB + q]);
+    }
+    uv[t] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < (KB * KB + NTHR - 1) / NTHR; ++t) {
+    const int e = tid + t * NTHR;
+    if (e < KB * KB) u12[e] = uv[t];
+  }
+  __syncthreads();
+  // this panel's rows: interchanged block row minus L21 U12.  With a stage (the caller's
+  // per-thread smem slots, stride RPT*NTHR) one row is live at a time and the frame is loaded
+  // afterwards, so the update does not add to the column loop's register pressure.
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    T v[KB];
+    if (!alive[j]) {
+#pragma unroll
+      for (int q = 0; q < KB; ++q) v[q] = zero_of<T>();
+    } else {
+      const int r = k0 + myrow[j];
+      const T* src = A + (int64_t)src_of(r) + (int64_t)lda * k0;
+#pragma unroll
+      for (int q = 0; q < KB; ++q) v[q] = q < kb ? src[(int64_t)lda * q] : zero_of<T>();
+      const T* lrow = A + (int64_t)r + (int64_t)lda * pv.kp0;
+#pragma unroll 1
+      for (int p0 = 0; p0 < pv.kbp; p0 += 8) {
+        T l[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) l[p] = (p0 + p < pv.kbp) ? lrow[(int64_t)lda * (p0 + p)] : zero_of<T>();
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const T* ur = u12 + (p0 + p) * KB;
+#pragma unroll
+          for (int q = 0; q < KB; ++q) fms_acc(v[q], l[p], ur[q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      if (stage) stage[(size_t)q * RPT * NTHR + j * NTHR + tid] = v[q];
+      else a[j][q] = v[q];
+    }
+  }
+  if (stage) {
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+#pragma unroll
+      for (int q = 0; q < KB; ++q) a[j][q] = stage[(size_t)q * RPT * NTHR + j * NTHR + tid];
+  }
+}
+
+// rank 0 of the cluster, after the column loop: U12 into the step's top rows of this block
+template <class T, int NTHR>
+__device__ __forceinline__ void panel_prev_store(T* __restrict__ A, int lda, int k0, int kb, const PanelPrev<T>& pv,
+                                                 const T* u12) {
+  constexpr int KB = kLuMaxKB;
+  if (pv.kp0 < 0) return;
+  for (int e = threadIdx.x; e < KB * KB; e += NTHR) {
+    const int i = e % KB, q = e / KB;
+    if (i < pv.kbp && q < kb) A[(int64_t)(pv.kp0 + i) + (int64_t)lda * (k0 + q)] = u12[i * KB + q];
+  }
+}
+
 template <class T, int KB, int RPT, int NTHR>
 __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n, int lda, int k0, int kb, LuWork w,
-                                                       T* __restrict__ invL, const LmDeviceState* st, int gate_running) {
+                                                       T* __restrict__ invL, const LmDeviceState* st, int gate_running,
+                                                       PanelPrev<T> pv) {
+  static_assert(KB == kLuMaxKB, "panel width");
   if (st && gate_running && (st->stopped || st->err_code)) return;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
@@ -104,10 +228,9 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
   for (int j = 0; j < RPT; ++j) {
     myrow[j] = rank * cta_rows + j * NTHR + tid;
     alive[j] = myrow[j] < m;
-    const T* src = A + (int64_t)(k0 + myrow[j]) + (int64_t)lda * k0;
-#pragma unroll
-    for (int q = 0; q < KB; ++q) a[j][q] = (alive[j] && q < kb) ? src[(int64_t)lda * q] : zero_of<T>();
   }
+  // PanelPrev scratch: gather list in pivrows..misc (4 KB ints), U12 in top (both used only later)
+  panel_load<T, RPT, NTHR>(a, A, lda, k0, kb, myrow, alive, pv, pivrows, top);
   T cur[RPT];  // a[j][jj] of the current column, maintained by the elimination loop
 #pragma unroll
   for (int j = 0; j < RPT; ++j) cur[j] = a[j][0];
@@ -119,6 +242,10 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
     fence_mbar_init();
   }
   cluster.sync();  // remote CTAs may target pbar only once it is initialised
+  if (rank == 0) {  // every CTA is past its loads: U12 to the previous step's top rows
+    panel_prev_store<T, NTHR>(A, lda, k0, kb, pv, top);
+    __syncthreads();  // top is reused for the pivot rows
+  }
   const uint32_t pk_tx = (uint32_t)(NC * PK::PKC * 16);
 
   // Column loop NOT unrolled (I-cache); registers addressed statically by predication over q.

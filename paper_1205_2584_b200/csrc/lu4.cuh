@@ -37,7 +37,8 @@ size_t panel4_smem_bytes(int CL, int nthr, int rpt) {
 
 template <class T, int RPT, int NTHR>
 __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n, int lda, int k0, int kb, LuWork w,
-                                                       T* __restrict__ invL, const LmDeviceState* st, int gate_running) {
+                                                       T* __restrict__ invL, const LmDeviceState* st, int gate_running,
+                                                       PanelPrev<T> pv) {
   if (st && gate_running && (st->stopped || st->err_code)) return;
   constexpr int KB = kLuMaxKB;  // 32
   constexpr int CH = 8;         // columns per static chunk
@@ -71,16 +72,16 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
     myrow[j] = rank * ROWS + j * NTHR + tid;
     alive[j] = myrow[j] < m;
     pcol[j] = -1;
-    const T* src = A + (int64_t)(k0 + myrow[j]) + (int64_t)lda * k0;
-#pragma unroll
-    for (int q = 0; q < KB; ++q) a[j][q] = (alive[j] && q < kb) ? src[(int64_t)lda * q] : zero_of<T>();
   }
+  // PanelPrev scratch: gather list in pivrows..misc, U12 in top, rows staged in fin (all used later)
+  panel_load<T, RPT, NTHR>(a, A, lda, k0, kb, myrow, alive, pv, pivrows, top, fin);
   if (tid == 0) {
     mbar_init(&pbar[0], 1);
     mbar_init(&pbar[1], 1);
     fence_mbar_init();
   }
   cluster.sync();  // remote CTAs may target pbar only once it is initialised
+  if (rank == 0) panel_prev_store<T, NTHR>(A, lda, k0, kb, pv, top);  // every CTA is past its loads
   const uint32_t pk_tx = (uint32_t)(CL * PK::PKC * 16);
   const uint32_t bar0_u32 = smem_u32(&pbar[0]), bar1_u32 = smem_u32(&pbar[1]);
 
