@@ -132,6 +132,13 @@ int cpf_engine_phase_times(cpf_engine* e, double* ms_out, int64_t* counts_out, i
 int cpf_engine_unfolding_gram(cpf_engine* e, int mode, void* out);
 /* Number of kernels this engine has launched (for the bench's gpu_launches count). */
 int64_t cpf_engine_launch_count(const cpf_engine* e);
+/* Tensor-pass implementation the engine planned for its tensor (diagnostic, no reference
+ * counterpart): fp64/complex FMA passes, fp64 tensor-core DMMA passes, or the int8 tcgen05 passes
+ * on exact digit splits (Ozaki scheme). */
+#define CPF_PASS_FMA 0
+#define CPF_PASS_DMMA 1
+#define CPF_PASS_OZAKI 2
+int cpf_engine_pass_impl(const cpf_engine* e);
 
 #ifdef __cplusplus
 }

@@ -31,6 +31,11 @@ CPF_E_STATE = -8
 CPF_REAL = 0
 CPF_COMPLEX = 1
 
+# tensor-pass implementations (cpf_engine_pass_impl)
+PASS_FMA = 0
+PASS_DMMA = 1
+PASS_OZAKI = 2
+
 VARIANT_CODE = {"auto": 0, "flm-a": 1, "flm-b": 2}
 
 STOP_RUNNING = 0
@@ -77,6 +82,7 @@ EXPORTED_SYMBOLS = (
     "cpf_engine_phase_times",
     "cpf_engine_launch_count",
     "cpf_engine_unfolding_gram",
+    "cpf_engine_pass_impl",
 )
 
 
@@ -123,6 +129,7 @@ def _declare(lib) -> None:
         "cpf_engine_phase_times": (I, [P, ctypes.POINTER(D), ctypes.POINTER(I64), I]),
         "cpf_engine_launch_count": (I64, [P]),
         "cpf_engine_unfolding_gram": (I, [P, I, P]),
+        "cpf_engine_pass_impl": (I, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -303,3 +310,6 @@ class Engine:
 
     def launch_count(self) -> int:
         return int(self._lib.cpf_engine_launch_count(self._h))
+
+    def pass_impl(self) -> int:
+        return int(self._lib.cpf_engine_pass_impl(self._h))

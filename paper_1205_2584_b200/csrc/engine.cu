@@ -37,6 +37,7 @@ struct ApiError : std::runtime_error {
 #include "tensor_pass.cuh"
 #include "tensor_pass2.cuh"
 #include "tensor_pass_dmma.cuh"
+#include "tensor_pass_oz.cuh"
 
 #define NCCL_CHECK(expr)                                                                   \
   do {                                                                                     \
@@ -73,6 +74,7 @@ struct EngineBase {
   virtual void profile(int on) = 0;
   virtual void phase_times(double* ms, int64_t* cnt, int n) = 0;
   virtual int64_t launches() const = 0;
+  virtual int pass_impl() const = 0;
   virtual void unfolding_gram(int mode, void* out) = 0;
 };
 
@@ -131,6 +133,12 @@ struct Engine final : EngineBase {
   int64_t pb_mper = 1;
   // DMMA (fp64 tensor core) passes for float64 with large I1
   bool use_dmma = false;
+  // Ozaki-split int8 tensor passes (tensor_pass_oz.cuh): real tensors, I1 >= 256, R <= 32, large J
+  bool use_oz = false;
+  OzGeom oa{}, ob{};
+  uint8_t *ozYA = nullptr, *ozYB = nullptr, *ozBA = nullptr, *ozBB = nullptr;
+  int *ozFrowA = nullptr, *ozFrowB = nullptr, *ozFr = nullptr;  // ozFr: [0, 32) pass A, [32, 64) pass B
+  double *ozM1 = nullptr, *ozZ = nullptr, *ozBp = nullptr;          // epilogue partial sums
   int dm_nt = 0;
   DmmaGeom da{}, db{};
   size_t da_smem = 0, db_smem = 0;
@@ -242,7 +250,8 @@ struct Engine final : EngineBase {
     for (auto& e : evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     void* ptrs[] = {Yown, A, Ac, M, Mc, D, G, Cand, V1, V2, V3, V4, Cg, Ccg, Gx, Gp, Gf, Gti, Gi, W1, Sm,
                     wvec, fvec, xvec, Phi, A1c, KMc, WNc, A1r, KMr, WNr, zpart, m1part, bpart, pa_out, pb_out, pb_all,
-                    norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL, WNd, KMd, gring, PhiInv, TriTmp, yvec, tmv_part};
+                    norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL, WNd, KMd, gring, PhiInv, TriTmp, yvec, tmv_part,
+                    ozYA, ozYB, ozBA, ozBB, ozFrowA, ozFrowB, ozFr, ozM1, ozZ, ozBp};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (hst) cudaFreeHost(hst);
@@ -364,6 +373,7 @@ struct Engine final : EngineBase {
     plan_lu3();
     plan_v2(nsm);
     plan_dmma(nsm);
+    plan_oz();
     CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lu_smem));
     if (lu_cl > 8) CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     set_pass_attrs();
@@ -472,6 +482,49 @@ struct Engine final : EngineBase {
       case 6: f(IC<6>{}); break;
       case 8: f(IC<8>{}); break;
       default: throw ApiError(CPF_E_UNSUPPORTED, "unsupported DMMA n-tile count");
+    }
+  }
+
+  // Ozaki passes: chosen for large real tensors (config 4: 2.45 ms per pass instead of 3.3 ms on
+  // DMMA); CPF_OZ=1 forces them for any real tensor with R <= 32 (tests), CPF_OZ=0 disables.
+  void plan_oz() {
+    use_oz = false;
+    if constexpr (sizeof(T) != 8) return;
+    else {
+      const char* e = getenv("CPF_OZ");
+      const bool force = e && e[0] == '1';
+      if (e && e[0] == '0') return;
+      // int32 accumulators: 8 pairs x 127^2 per K element -> K <= 16384 per contraction
+      if (R > kOzN || Cloc < 1 || Cloc > 16384 || Lmid > 16384) return;
+      if (!force && (I1 < 256 || Jloc < ((int64_t)1 << 26))) return;
+      const int nb = (int)((I1 + kOzM - 1) / kOzM);
+      oa = OzGeom{I1, Lmid, Cloc, nb, (int)((Cloc + kOzK - 1) / kOzK), Lmid, (int64_t)nb * Lmid, R, 0};
+      ob = OzGeom{I1, Lmid, Cloc, nb, (int)((Lmid + kOzK - 1) / kOzK), Cloc, (int64_t)nb * Cloc, R, 0};
+      ozYA = dalloc<uint8_t>((size_t)oa.ntiles * oa.nkb * kOzABytes);
+      ozYB = dalloc<uint8_t>((size_t)ob.ntiles * ob.nkb * kOzABytes);
+      ozFrowA = dalloc<int>((size_t)oa.ntiles * kOzM);
+      ozFrowB = dalloc<int>((size_t)ob.ntiles * kOzM);
+      ozBA = dalloc<uint8_t>((size_t)oa.nkb * kOzBBytes);  // zero: padding columns / K tail
+      ozBB = dalloc<uint8_t>((size_t)ob.nkb * kOzBBytes);
+      ozFr = dalloc<int>(2 * kOzN);
+      ozM1 = dalloc<double>((size_t)std::max(1, nsm_ / nb) * I1 * RP);
+      ozZ = dalloc<double>((size_t)nb * Lmid * RP);
+      ozBp = dalloc<double>((size_t)Cloc * nb * RP);
+      CPF_CUDA_CHECK(cudaFuncSetAttribute(k_oz_pass<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOzSmem));
+      CPF_CUDA_CHECK(cudaFuncSetAttribute(k_oz_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOzSmem));
+      use_oz = true;
+    }
+  }
+  // one-time digit-plane images of the bound tensor (both passes), stream-ordered after the upload
+  void oz_split() {
+    if (!use_oz || Jloc == 0) return;
+    if constexpr (sizeof(T) == 8) {
+      const double* Yd = reinterpret_cast<const double*>(Y);
+      k_oz_rowexp<0><<<nsm_ * 8, 256, 0, s>>>(Yd, oa, ozFrowA);
+      k_oz_split_y<0><<<nsm_ * 16, 256, 0, s>>>(Yd, oa, ozFrowA, ozYA);
+      k_oz_rowexp<1><<<nsm_ * 8, 256, 0, s>>>(Yd, ob, ozFrowB);
+      k_oz_split_y<1><<<nsm_ * 16, 256, 0, s>>>(Yd, ob, ozFrowB, ozYB);
+      CPF_CUDA_CHECK(cudaGetLastError());
     }
   }
 
@@ -687,6 +740,20 @@ struct Engine final : EngineBase {
     prep_operands(F, true, gate);
     ph_begin(kPhPassA);
     if constexpr (sizeof(T) == 8) {
+      if (Cloc > 0 && use_oz) {
+        const LmDeviceState* cst = st;
+        const DevFlags* cfl = fl;
+        launch(k_oz_split_b, dim3(R), 256, 0, (const double*)WNc, Cloc, R, RP, ozBA, ozFr, cst, cfl, gate);
+        const int nch = std::max(1, nsm_ / oa.nb);
+        const OzOut oo{(const double*)A1c, (const double*)KMc, RP, nch, (Lmid + nch - 1) / nch, ozM1, ozZ};
+        launch(k_oz_pass<0>, dim3((unsigned)(oa.nb * nch)), kOzThreads, kOzSmem, (const uint8_t*)ozYA,
+               (const int*)ozFrowA, (const uint8_t*)ozBA, (const int*)ozFr, oa, oo, cst, cfl, gate);
+        ph_end();
+        launch(k_m1_reduce<T>, nblocks(I1 * R, 32), 256, 0, (const T*)ozM1, nch, I1, R, RP, pa_out, cst, cfl, gate);
+        launch(k_z_reduce<T>, nblocks(Lmid * R, 256), 256, 0, (const T*)ozZ, oa.nb, Lmid, R, RP, pa_out + I1 * R,
+               cst, cfl, gate);
+        goto pass_a_done;
+      }
       if (Cloc > 0 && use_dmma) {
         const LmDeviceState* cst = st;
         const DevFlags* cfl = fl;
@@ -757,9 +824,22 @@ struct Engine final : EngineBase {
     prep_operands(F, false, gate);
     ph_begin(kPhPassB);
     int nparts = pb_chunks * pb_tiles;
-    bool done_b = false;
+    bool done_b = false, oz_b = false;
     if constexpr (sizeof(T) == 8) {
-      if (Cloc > 0 && use_dmma) {
+      if (Cloc > 0 && use_oz) {
+        // overlapped with the next LU (ls != s): leave kLuReserveSms SMs to the panel clusters
+        const int grid = ls != s ? std::max(1, nsm_ - kLuReserveSms) : nsm_;
+        launch(k_oz_split_b, dim3(R), 256, 0, (const double*)KMc, Lmid, R, RP, ozBB, ozFr + kOzN,
+               (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+        const int nch = std::max(1, grid / ob.nb);
+        const OzOut oo{(const double*)A1c, nullptr, RP, nch, (Cloc + nch - 1) / nch, nullptr, ozBp};
+        launch(k_oz_pass<1>, dim3((unsigned)(ob.nb * nch)), kOzThreads, kOzSmem, (const uint8_t*)ozYB,
+               (const int*)ozFrowB, (const uint8_t*)ozBB, (const int*)(ozFr + kOzN), ob, oo, (const LmDeviceState*)st,
+               (const DevFlags*)fl, gate);
+        nparts = ob.nb;
+        done_b = oz_b = true;
+      }
+      if (Cloc > 0 && use_dmma && !oz_b) {
         const LmDeviceState* cst = st;
         const DevFlags* cfl = fl;
         nparts = db_chunks * db.tiles;
@@ -808,14 +888,16 @@ struct Engine final : EngineBase {
       });
     }
     ph_end();
+    // M_N rows of this slab from the partial sums (Ozaki passes: one partial per i1 block)
+    auto mn_rows = [&](T* dst, int64_t ldm) {
+      launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, oz_b ? (const T*)ozBp : (const T*)bpart, Cloc,
+             nparts, R, RP, ldm, dst, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    };
     if (!comm) {
-      launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, (const T*)bpart, Cloc, nparts, R, RP,
-             IN, Mout + offs[N - 1], (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+      mn_rows(Mout + offs[N - 1], IN);
     } else {
       CPF_CUDA_CHECK(cudaMemsetAsync(pb_out, 0, sizeof(T) * Cpad * R, ls));
-      if (Cloc > 0)
-        launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, (const T*)bpart, Cloc, nparts, R, RP,
-               Cpad, pb_out, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+      if (Cloc > 0) mn_rows(pb_out, Cpad);
       const size_t cnt = (size_t)Cpad * R * (sizeof(T) / sizeof(double));
       NCCL_CHECK(ncclAllGather(pb_out, pb_all, cnt, ncclDouble, comm, ls));
       // pb_all[rank][c + Cpad r] -> Mout_N[(rank*Cpad + c) + IN r]
@@ -1208,6 +1290,7 @@ struct Engine final : EngineBase {
       if (Jloc > 0) CPF_CUDA_CHECK(cudaMemcpyAsync(Yown, p, Jloc * sizeof(T), cudaMemcpyHostToDevice, s));
       Y = Yown;
     }
+    oz_split();
     have_tensor = true;
   }
   void set_factors(const void* p) override {
@@ -1449,6 +1532,7 @@ struct Engine final : EngineBase {
     }
   }
   int64_t launches() const override { return nlaunch; }
+  int pass_impl() const override { return use_oz ? CPF_PASS_OZAKI : use_dmma ? CPF_PASS_DMMA : CPF_PASS_FMA; }
 
   // G_n = Y_(n) Y_(n)^H on the device (sum of the slab partials across ranks for n < N)
   void unfolding_gram(int mode, void* out) override {
@@ -1628,6 +1712,7 @@ int cpf_engine_phase_times(cpf_engine* e, double* ms_out, int64_t* counts_out, i
 }
 
 int64_t cpf_engine_launch_count(const cpf_engine* e) { return (e && e->impl) ? e->impl->launches() : 0; }
+int cpf_engine_pass_impl(const cpf_engine* e) { return (e && e->impl) ? e->impl->pass_impl() : -1; }
 
 int cpf_engine_unfolding_gram(cpf_engine* e, int mode, void* out) {
   if (!e || !e->impl) return CPF_E_STATE;
