@@ -317,7 +317,8 @@ struct Engine final : EngineBase {
   // Launch geometry for the tensor passes and the LU panel.
   int nsm_ = 148;
   // SMs left to the LU while pass B runs alongside it (CPF_LU_RESERVE overrides)
-  const int kLuReserveSms = [] { const char* e = getenv("CPF_LU_RESERVE"); return e ? atoi(e) : 24; }();
+  // (HBM-bound Ozaki pass B: 40, measured best of 24..48 at config 4; DMMA pass B: 24)
+  int kLuReserveSms = 24;
   // pass B overlapped with the LU runs as a persistent grid on nsm - kLuReserveSms SMs, so the LU's
   // small panel clusters and GEMM updates always find free SMs (CPF_PERSISTENT_B=0: plain grid)
   const bool persistent_b = [] { const char* e = getenv("CPF_PERSISTENT_B"); return !(e && e[0] == '0'); }();
@@ -374,6 +375,8 @@ struct Engine final : EngineBase {
     plan_v2(nsm);
     plan_dmma(nsm);
     plan_oz();
+    kLuReserveSms = use_oz ? 40 : 24;
+    if (const char* e = getenv("CPF_LU_RESERVE")) kLuReserveSms = atoi(e);
     CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lu_smem));
     if (lu_cl > 8) CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     set_pass_attrs();
@@ -500,6 +503,9 @@ struct Engine final : EngineBase {
       const int nb = (int)((I1 + kOzM - 1) / kOzM);
       oa = OzGeom{I1, Lmid, Cloc, nb, (int)((Cloc + kOzK - 1) / kOzK), Lmid, (int64_t)nb * Lmid, R, 0};
       ob = OzGeom{I1, Lmid, Cloc, nb, (int)((Lmid + kOzK - 1) / kOzK), Cloc, (int64_t)nb * Cloc, R, 0};
+      // pass A streams alone: no L2 hint (measured 3 % faster); pass B runs beside the LU: evict-first
+      oa.dbg = 4;
+      if (const char* d = getenv("CPF_OZ_DBG")) oa.dbg = ob.dbg = atoi(d);  // experiments
       ozYA = dalloc<uint8_t>((size_t)oa.ntiles * oa.nkb * kOzABytes);
       ozYB = dalloc<uint8_t>((size_t)ob.ntiles * ob.nkb * kOzABytes);
       ozFrowA = dalloc<int>((size_t)oa.ntiles * kOzM);

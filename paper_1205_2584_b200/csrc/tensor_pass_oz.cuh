@@ -68,7 +68,7 @@ struct OzGeom {
   int64_t nouter;       // MODE 0: Lmid, MODE 1: C
   int64_t ntiles;       // nb * nouter; tile t = outer * nb + i1 block
   int R;
-  int dbg;              // experiments: bit 0 = no output stores, bit 1 = no MMAs
+  int dbg;              // experiments: bit 0 = no output stores, bit 1 = no MMAs, bit 2 = no L2 hint
 };
 
 __device__ __forceinline__ int oz_scale_exp(double amax) {
@@ -211,6 +211,22 @@ __device__ __forceinline__ void oz_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// streaming bulk copy with an L2 evict-first policy: the 16 GB image stream should not push the
+// concurrently running LU's matrix (11.5 MB) and the B operands out of L2
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 __device__ __forceinline__ void oz_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -300,13 +316,15 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     if (lane == 0) {  // ---- bulk-copy producer
       int s = 0;
       uint32_t ph = 0;
+      const uint64_t pol = policy_evict_first();
       for (int64_t o = obeg; o < oend; ++o) {
         const int64_t t = o * g.nb + b;
         for (int kb = 0; kb < g.nkb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1u);
           unsigned char* sa = base + (size_t)s * kOzStageBytes;
           mbar_expect_tx(&full[s], kOzStageBytes);
-          bulk_g2s(sa, Yimg + (size_t)(t * g.nkb + kb) * kOzABytes, kOzABytes, &full[s]);
+          if (g.dbg & 4) bulk_g2s(sa, Yimg + (size_t)(t * g.nkb + kb) * kOzABytes, kOzABytes, &full[s]);
+          else bulk_g2s_stream(sa, Yimg + (size_t)(t * g.nkb + kb) * kOzABytes, kOzABytes, &full[s], pol);
           bulk_g2s(sa + kOzABytes, Bq + (size_t)kb * kOzBBytes, kOzBBytes, &full[s]);
           if (++s == kOzStages) { s = 0; ph ^= 1u; }
         }
