@@ -267,9 +267,15 @@ def main():
             traffic = json.loads(prof_json.read_text()).get(args.config)
         except Exception:
             traffic = None
+    impl = eng.pass_impl()
+    kname = {_native.PASS_OZAKI: "k_oz_pass<0>: pass A (MTTKRP modes 1..N-1 + trial-fit contraction) on the int8 "
+                                 "tensor cores, exact 8-digit split of the fp64 operands (tcgen05 kind::i8)",
+             _native.PASS_DMMA: "k_pass_dmma<NT,0>: pass A (MTTKRP modes 1..N-1 + trial-fit contraction) on the "
+                                "fp64 tensor cores (DMMA)",
+             _native.PASS_FMA: "k_pass_a2: pass A (MTTKRP modes 1..N-1 + trial-fit contraction), fp64 FMA"}[impl]
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
-                "kernel": "k_pass_a (MTTKRP modes 1..N-1 + trial-fit contraction)",
+                "kernel": kname,
                 "bytes_per_launch": bytes_a, "avg_launch_ms": round(t_a, 4), "launches": na,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})",
                 "share_of_step": round(((ms1[0] - ms0[0]) / np_done) / (ms / max(iters_done, 1)), 4) if ms > 0 else None,
