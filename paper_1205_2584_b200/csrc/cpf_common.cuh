@@ -207,6 +207,17 @@ struct IterRecordDev {
 // TMA bulk copies (cp.async.bulk, 1-D) + mbarrier pipeline helpers (sm_90+/sm_100a)
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// Programmatic dependent launch.  Kernels of the iteration graph are launched with programmatic
+// stream serialization: kernel n+1 may be scheduled while kernel n still runs.  Every kernel starts
+// here: wait until the predecessor grid has completed and its memory is visible, then let the
+// successor be scheduled (its CTAs park in their own wait).  Launch latency of a chain of small
+// dependent kernels overlaps the previous kernel instead of adding to it.  No-op for a normally
+// launched kernel.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }

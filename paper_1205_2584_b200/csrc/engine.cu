@@ -326,6 +326,11 @@ struct Engine final : EngineBase {
   // GEMM launches between consecutive panels.  Measured (1 x B200): C1 43.3 -> 51.1 it/s, C2 359 ->
   // 405, C4 131.4 -> 131.4 (there the LU is hidden behind pass B).  CPF_LU_FUSE=0: unfused.
   bool lu_fuse = true;
+  // programmatic dependent launch for the launch() helper's kernels (CPF_PDL=0: off)
+  // Only the single-stream chain from the candidate to the commit uses it: in the fork (pass B beside
+  // the LU) early-scheduled CTAs would park on the SMs left to the LU (measured 162 -> 140 it/s).
+  const bool use_pdl = [] { const char* e = getenv("CPF_PDL"); return !(e && e[0] == '0'); }();
+  bool pdl_now = false;
   void plan() {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -663,7 +668,21 @@ struct Engine final : EngineBase {
   template <class K, class... Args>
   void launch(K kern, dim3 g, dim3 b, size_t smem, Args... args) {
     if (g.x == 0 || g.y == 0 || g.z == 0) return;
-    kern<<<g, b, smem, ls>>>(args...);
+    if (use_pdl && pdl_now) {  // programmatic dependent launch (pdl_wait, cpf_common.cuh)
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = g;
+      cfg.blockDim = b;
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = ls;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, args...));
+    } else {
+      kern<<<g, b, smem, ls>>>(args...);
+    }
     ++nlaunch;
     CPF_CUDA_CHECK(cudaGetLastError());
   }
@@ -1384,6 +1403,7 @@ struct Engine final : EngineBase {
 
   void iteration() {
     const int g = kRunning;
+    pdl_now = true;
     candidate(2, g, /*core_ready=*/true);  // Phi(mu_t, cache_t) was factored at the end of t-1
     // delta' = cand - model (solver.py:348)
     axpby(Cand, 1.0, A, -1.0, V1, g);
@@ -1410,6 +1430,7 @@ struct Engine final : EngineBase {
            (const DevFlags*)fl, ga);
     // fork: pass B (M_N of the new model) + gradient on s3, while s factors the next step's
     // core system Phi(mu_{t+1}, cache_{t+1}) -- independent of Y, so the two overlap
+    pdl_now = false;
     if (serial) {  // diagnostic (CPF_SERIAL=1): no overlap, phases time standalone
       pass_b(A, M, ga);
       gradient(ga);

@@ -41,6 +41,7 @@ struct LuWork {
 };
 
 __global__ void k_lu_init(int* perm, int n, int* info) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) perm[i] = i;
   if (i == 0) *info = 0;
@@ -49,6 +50,7 @@ __global__ void k_lu_init(int* perm, int n, int* info) {
 template <class T>
 __global__ void __launch_bounds__(256) k_panel_lu(T* __restrict__ A, int n, int lda, int k0, int kb, int rpc, LuWork w,
                                                   const LmDeviceState* st, int gate_running) {
+  pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
@@ -203,6 +205,7 @@ size_t panel_smem_bytes(int rpc, int kb, int CL) {
 template <class T>
 __global__ void k_row_gather(T* __restrict__ A, int n, int lda, int k0, int kb, LuWork w, const LmDeviceState* st,
                              int gate_running) {
+  pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int G = *w.gcount;
@@ -237,6 +240,7 @@ template <class T>
 __global__ void k_row_gather2(T* __restrict__ A, int lda, const int* __restrict__ gather, const int* __restrict__ gcount,
                               int* __restrict__ perm, int ca0, int ca1, int cb0, int cb1, int do_perm,
                               const LmDeviceState* st, int gate_running) {
+  pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int G = *gcount;
@@ -268,6 +272,7 @@ __global__ void k_row_gather2(T* __restrict__ A, int lda, const int* __restrict_
 template <class T, int KB>
 __global__ void k_trsm_llnu(T* __restrict__ A, int n, int lda, int k0, int kb, const LmDeviceState* st,
                             int gate_running) {
+  pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
   __shared__ T L[KB * KB];
   for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
@@ -298,6 +303,7 @@ __global__ void k_trsm_llnu(T* __restrict__ A, int n, int lda, int k0, int kb, c
 template <class T>
 __global__ void __launch_bounds__(256) k_gemm_sub(T* __restrict__ Mx, int lda, int r0, int c0, int k0, int m, int nn,
                                                   int k, const LmDeviceState* st, int gate_running) {
+  pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
   constexpr int TM = 64, TN = 64, BK = 16;
   __shared__ T As[BK][TM + 1];
@@ -350,6 +356,7 @@ __global__ void __launch_bounds__(256) k_gemm_sub(T* __restrict__ Mx, int lda, i
 
 // LU info -> engine error code (flm-a singular maps to the "I + Psi K" message)
 __global__ void k_lu_info_to_err(const int* info, LmDeviceState* st) {
+  pdl_wait();
   if (st->stopped || st->err_code) return;
   if (*info != 0) st->err_code = st->use_kinv ? kErrSingular : kErrPhi1Singular;
 }
@@ -358,6 +365,7 @@ __global__ void k_lu_info_to_err(const int* info, LmDeviceState* st) {
 template <class T>
 __global__ void k_perm_gather(const T* __restrict__ b, const int* __restrict__ perm, int n, T* __restrict__ x,
                               const LmDeviceState* st, int gate_running) {
+  pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
   int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q < n) x[q] = b[perm[q]];
@@ -400,6 +408,7 @@ template <class T, bool LOWER>
 __global__ void __launch_bounds__(128) k_trsv(const T* __restrict__ A, int n, int lda, T* __restrict__ x,
                                               int* __restrict__ ticket, int* __restrict__ ready, int epoch,
                                               const LmDeviceState* st, int gate_running) {
+  pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
   __shared__ int s_b;
   __shared__ T part[4][32];

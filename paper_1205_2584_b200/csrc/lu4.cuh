@@ -39,6 +39,7 @@ template <class T, int RPT, int NTHR>
 __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n, int lda, int k0, int kb, LuWork w,
                                                        T* __restrict__ invL, const LmDeviceState* st, int gate_running,
                                                        PanelPrev<T> pv) {
+  pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
   constexpr int KB = kLuMaxKB;  // 32
   constexpr int CH = 8;         // columns per static chunk

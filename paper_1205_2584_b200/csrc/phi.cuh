@@ -19,6 +19,7 @@ template <class T>
 __global__ void k_phi_assemble(T* __restrict__ Phi, int N, int R, const T* __restrict__ Cg,
                                const T* __restrict__ Gi, const T* __restrict__ pair, const T* __restrict__ full,
                                const LmDeviceState* st, int gate_running) {
+  pdl_wait();
   if (gate_running && st->stopped) return;
   if (st->err_code) return;
   const int R2 = R * R;
@@ -64,6 +65,7 @@ __global__ void k_phi_assemble(T* __restrict__ Phi, int N, int R, const T* __res
 template <class T>
 __global__ void k_apply_k(const T* __restrict__ z, int N, int R, const T* __restrict__ pair, T* __restrict__ f,
                           const LmDeviceState* st, int gate_running) {
+  pdl_wait();
   if (gate_running && st->stopped) return;
   if (st->err_code) return;
   const int R2 = R * R;

@@ -48,6 +48,7 @@ __device__ __forceinline__ bool gate_open(const LmDeviceState* st, const DevFlag
 template <class T>
 __global__ void k_cross_gram(const T* __restrict__ X, const T* __restrict__ Yv, Modes md, T* __restrict__ out,
                              const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   __shared__ T scratch[32];
   const int n = blockIdx.y;
@@ -68,6 +69,7 @@ __global__ void k_cross_gram(const T* __restrict__ X, const T* __restrict__ Yv, 
 template <class T>
 __global__ void k_hadamards(const T* __restrict__ Cg, int N, int R, T* __restrict__ excl, T* __restrict__ pair,
                             T* __restrict__ full, const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const int R2 = R * R;
@@ -97,6 +99,7 @@ __global__ void k_hadamards(const T* __restrict__ Cg, int N, int R, T* __restric
 template <class T>
 __global__ void k_kernel_flag(const T* __restrict__ pair, int N, int R, LmDeviceState* st, const DevFlags* fl,
                               int gate, int* kinv_ok_out) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   __shared__ double smax[32], smin[32];
   const int R2 = R * R;
@@ -137,6 +140,7 @@ template <class T>
 __global__ void k_damped_inverses(const T* __restrict__ excl, int N, int R, T* __restrict__ Gti, T* __restrict__ Gi,
                                   LmDeviceState* st, const DevFlags* fl, int gate, const int* kinv_ok,
                                   const double* mu_override) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* a = reinterpret_cast<T*>(smem_raw);  // R x 2R augmented, column-major (ld = R)
@@ -222,6 +226,7 @@ struct TallArgs {
 
 template <class T>
 __global__ void k_tall(TallArgs a, Modes md, const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int R = md.R;
@@ -276,6 +281,7 @@ __global__ void k_tall(TallArgs a, Modes md, const LmDeviceState* st, const DevF
 template <class T>
 __global__ void k_axpby(const T* __restrict__ x, double alpha, const T* __restrict__ y, double beta, T* __restrict__ out,
                         int64_t n, const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -297,6 +303,7 @@ template <class T>
 __global__ void k_small(int op, const T* __restrict__ P0, const T* __restrict__ P1, const T* __restrict__ excl,
                         const T* __restrict__ Gti, const T* __restrict__ pair, int N, int R, T* __restrict__ out,
                         const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int R2 = R * R;
@@ -369,6 +376,7 @@ __global__ void k_small(int op, const T* __restrict__ P0, const T* __restrict__ 
 template <class T>
 __global__ void k_colnorms(const T* __restrict__ X, Modes md, double* __restrict__ norms, const LmDeviceState* st,
                            const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   __shared__ double scratch[32];
   const int n = blockIdx.y, r = blockIdx.x;
@@ -388,6 +396,7 @@ __global__ void k_colnorms(const T* __restrict__ X, Modes md, double* __restrict
 template <class T>
 __global__ void k_normalize(const T* __restrict__ X, Modes md, const double* __restrict__ norms, T* __restrict__ out,
                             LmDeviceState* st, const DevFlags* fl, int gate, int mode) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   __shared__ double sval[32];
   __shared__ long long sidx[32];
@@ -470,6 +479,7 @@ __global__ void k_normalize(const T* __restrict__ X, Modes md, const double* __r
 template <class T>
 __global__ void k_xnorm2(const T* __restrict__ Cg, int N, int R, double* __restrict__ outp, const LmDeviceState* st,
                          const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   __shared__ double scratch[32];
   const int R2 = R * R;
@@ -487,6 +497,7 @@ __global__ void k_xnorm2(const T* __restrict__ Cg, int N, int R, double* __restr
 template <class T>
 __global__ void k_redot(const T* __restrict__ a, const T* __restrict__ b, int64_t n, int with_mu,
                         double* __restrict__ outp, const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   __shared__ double scratch[32];
   const double mu = st->mu;
@@ -503,6 +514,7 @@ __global__ void k_redot(const T* __restrict__ a, const T* __restrict__ b, int64_
 // ||Y||^2 partials over a large buffer: grid-stride, per-block partial (fixed order)
 template <class T>
 __global__ void k_sumsq_partial(const T* __restrict__ y, int64_t n, double* __restrict__ part) {
+  pdl_wait();
   __shared__ double scratch[32];
   double acc = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -513,6 +525,7 @@ __global__ void k_sumsq_partial(const T* __restrict__ y, int64_t n, double* __re
 
 __global__ void k_sum_partials(const double* __restrict__ part, int n, double* __restrict__ outp,
                                const LmDeviceState* st = nullptr, const DevFlags* fl = nullptr, int gate = 0) {
+  pdl_wait();
   if (gate && !gate_open(st, fl, gate)) return;
   __shared__ double scratch[32];
   double acc = 0.0;
@@ -525,6 +538,7 @@ __global__ void k_sum_partials(const double* __restrict__ part, int n, double* _
 template <class T>
 __global__ void k_copy(const T* __restrict__ src, T* __restrict__ dst, int64_t n, const LmDeviceState* st,
                        const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[i] = src[i];
@@ -534,6 +548,7 @@ __global__ void k_copy(const T* __restrict__ src, T* __restrict__ dst, int64_t n
 template <class T>
 __global__ void k_copy2d(const T* __restrict__ src, int64_t lds, T* __restrict__ dst, int64_t ldd, int64_t rows,
                          int64_t cols, const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= rows * cols) return;
@@ -541,13 +556,15 @@ __global__ void k_copy2d(const T* __restrict__ src, int64_t lds, T* __restrict__
   dst[r * ldd + i] = src[r * lds + i];
 }
 
-__global__ void k_clear_pending(DevFlags* fl) { fl->pending_accept = 0; }
+__global__ void k_clear_pending(DevFlags* fl) {
+  pdl_wait(); fl->pending_accept = 0; }
 
 // Guard band: the identity ||Y||^2 - 2Re<Y,X> + ||X||^2 has an absolute error of a
 // few eps * ||Y||^2.  When the accept decision is within that band of a tie, or the residual is
 // so small that the identity cannot resolve it (exact-fit problems), the candidate's residual --
 // and, once, the current model's -- is recomputed directly from Y (k_direct_resid).
 __global__ void k_precheck(const LmDeviceState* st, DevFlags* fl, const double* scal) {
+  pdl_wait();
   if (st->stopped || st->err_code) {
     fl->need_direct = 0;
     fl->need_cur_direct = 0;
@@ -568,6 +585,7 @@ __global__ void k_precheck(const LmDeviceState* st, DevFlags* fl, const double* 
 // tolerance window and mu overflow.  scal[0] = Re<Y,X_cand>, scal[2] = ||X_cand||^2,
 // scal[3] = Re vdot(delta, g + mu delta).
 __global__ void k_decide(LmDeviceState* st, DevFlags* fl, IterRecordDev* trace, const double* scal) {
+  pdl_wait();
   if (st->stopped) return;
   const int t = st->iter + 1;
   if (st->err_code) {

@@ -26,6 +26,7 @@ template <class T>
 __global__ void k_conj_rowmajor(const T* __restrict__ src, int64_t rows, int64_t row0, int64_t ld, int R, int RP,
                                 T* __restrict__ dst, const LmDeviceState* st, const DevFlags* fl, int gate,
                                 int do_conj = 1) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= rows * RP) return;
@@ -45,6 +46,7 @@ struct MidGeom {
 template <class T>
 __global__ void k_krmid(const T* __restrict__ A, MidGeom g, int64_t Lmid, int R, int RP, T* __restrict__ dst,
                         const LmDeviceState* st, const DevFlags* fl, int gate, int do_conj = 1) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= Lmid * RP) return;
@@ -80,6 +82,7 @@ __global__ void __launch_bounds__(256) k_pass_a(const T* __restrict__ Y, int64_t
                                                 int TI, int TM, int64_t m_per_cta,
                                                 T* __restrict__ z_part, T* __restrict__ m1_part,
                                                 const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* w_s = reinterpret_cast<T*>(smem_raw);                 // kPassCK * RP
@@ -181,6 +184,7 @@ template <class T>
 __global__ void k_pass_a_reduce(const T* __restrict__ m1_part, int ngroups, const T* __restrict__ z_part, int ntiles,
                                 int64_t I1, int64_t Lmid, int R, int RP, T* __restrict__ M1, T* __restrict__ Z,
                                 const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n1 = I1 * R, n2 = Lmid * R;
@@ -210,6 +214,7 @@ __global__ void __launch_bounds__(256) k_pass_b(const T* __restrict__ Y, int64_t
                                                 const T* __restrict__ A1c, const T* __restrict__ KMc,
                                                 int TI, int TM, int64_t m_per_cta, T* __restrict__ part,
                                                 const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* red = reinterpret_cast<T*>(smem_raw);  // RP * (blockDim/32)
@@ -272,6 +277,7 @@ __global__ void __launch_bounds__(256) k_pass_b(const T* __restrict__ Y, int64_t
 template <class T>
 __global__ void k_pass_b_reduce(const T* __restrict__ part, int64_t C, int ng, int R, int RP, int64_t ldm,
                                 T* __restrict__ MN, const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= C * R) return;
@@ -286,6 +292,7 @@ __global__ void k_pass_b_reduce(const T* __restrict__ part, int64_t C, int ng, i
 template <class T>
 __global__ void k_mid_mttkrp(const T* __restrict__ Z, int64_t Lmid, const T* __restrict__ A, MidGeom g, int which,
                              int R, T* __restrict__ Mn, const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   const int64_t In = g.dims[which];
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -325,6 +332,7 @@ __global__ void __launch_bounds__(256) k_direct_resid(const T* __restrict__ Y, i
                                                       const T* __restrict__ WN, const T* __restrict__ A1r,
                                                       const T* __restrict__ KM, double* __restrict__ part,
                                                       const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* w_s = reinterpret_cast<T*>(smem_raw);

@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) k_pass_a2(const T* __restr
                                                     const T* __restrict__ A1c, const T* __restrict__ KMc,
                                                     T* __restrict__ z_part, T* __restrict__ m1_part,
                                                     const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // [0,NST) full, [NST,2NST) empty
@@ -219,6 +220,7 @@ template <class T, int RP, int RPT>
 __global__ void __launch_bounds__(kConsumers + 32, 1) k_pass_b2(const T* __restrict__ Y, PassGeom g, const T* __restrict__ A1c,
                                                     const T* __restrict__ KMc, T* __restrict__ part,
                                                     const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
@@ -334,6 +336,7 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) k_pass_b2(const T* __restr
 template <class T>
 __global__ void k_m1_reduce(const T* __restrict__ m1_part, int ngroups, int64_t I1, int R, int RP, T* __restrict__ M1,
                             const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   const int64_t o = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
   const int sub = threadIdx.x >> 5;  // 0..7
@@ -357,6 +360,7 @@ __global__ void k_m1_reduce(const T* __restrict__ m1_part, int ngroups, int64_t 
 template <class T>
 __global__ void k_z_reduce(const T* __restrict__ z_part, int ntiles, int64_t Lmid, int R, int RP, T* __restrict__ Z,
                            const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= Lmid * R) return;
@@ -379,6 +383,7 @@ namespace cpf {
 template <class T>
 __global__ void __launch_bounds__(256) k_unfold_gram(const T* __restrict__ Y, int64_t P, int64_t In, int64_t Q,
                                                      int64_t kchunk, T* __restrict__ part) {
+  pdl_wait();
   __shared__ T As[32][33];
   __shared__ T Bs[32][33];
   const int ntile = (int)((In + 31) / 32);
@@ -430,6 +435,7 @@ __global__ void __launch_bounds__(256) k_unfold_gram(const T* __restrict__ Y, in
 
 template <class T>
 __global__ void k_gram_reduce(const T* __restrict__ part, int nsplit, int64_t n2, T* __restrict__ G) {
+  pdl_wait();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n2) return;
   T s = part[e];

@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) k_pass_dmma(const double* 
                                                                   int RPg, int R, double* __restrict__ z_part,
                                                                   double* __restrict__ m1_part, const LmDeviceState* st,
                                                                   const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   constexpr int NCOL = 8 * NT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -281,6 +282,7 @@ __global__ void __launch_bounds__(kConsumers + 32, 1) k_pass_b_dmma_pers(const d
                                                                          double* __restrict__ part,
                                                                          const LmDeviceState* st, const DevFlags* fl,
                                                                          int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   constexpr int NCOL = 8 * NT;
   extern __shared__ __align__(128) unsigned char smem_raw[];

@@ -99,6 +99,7 @@ __device__ __forceinline__ int64_t oz_yidx(const OzGeom& g, int64_t i1, int64_t 
 // row exponents: thread per tile row (t, row); F = 0 for padding rows
 template <int MODE>
 __global__ void k_oz_rowexp(const double* __restrict__ Y, OzGeom g, int* __restrict__ Frow) {
+  pdl_wait();
   const int64_t K = MODE == 0 ? g.C : g.Lmid;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < g.ntiles * kOzM;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -117,6 +118,7 @@ __global__ void k_oz_rowexp(const double* __restrict__ Y, OzGeom g, int* __restr
 template <int MODE>
 __global__ void k_oz_split_y(const double* __restrict__ Y, OzGeom g, const int* __restrict__ Frow,
                              uint8_t* __restrict__ Yimg) {
+  pdl_wait();
   const int64_t K = MODE == 0 ? g.C : g.Lmid;
   const int64_t total = g.ntiles * g.nkb * (kOzK * kOzM / 4);
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -156,6 +158,7 @@ __global__ void k_oz_split_y(const double* __restrict__ Y, OzGeom g, const int* 
 // 8-row groups).  Columns r >= R and rows k >= K stay zero (buffer cleared at allocation).
 __global__ void k_oz_split_b(const double* __restrict__ src, int64_t K, int R, int ld, uint8_t* __restrict__ Bq,
                              int* __restrict__ Fr, const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   const int r = blockIdx.x;
   __shared__ double red[32];
@@ -276,6 +279,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kOzThreads, 1)
     k_oz_pass(const uint8_t* __restrict__ Yimg, const int* __restrict__ Frow, const uint8_t* __restrict__ Bq,
               const int* __restrict__ Fr, OzGeom g, OzOut out, const LmDeviceState* st, const DevFlags* fl, int gate) {
+  pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   extern __shared__ unsigned char oz_smem_raw[];
   unsigned char* base =

@@ -20,6 +20,7 @@ namespace cpf {
 template <class T>
 __global__ void __launch_bounds__(64) k_tri_inv_diag(const T* __restrict__ LU, int n, T* __restrict__ Inv,
                                                      const LmDeviceState* st, int gate_running) {
+  pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
   __shared__ T blk[32][33];
   const int b0 = blockIdx.x * 32;
@@ -81,6 +82,7 @@ __device__ __forceinline__ T tri_elem(const T* M, int n, int r, int c, int kind)
 template <class T, int STEP>
 __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* __restrict__ Inv, T* __restrict__ Tmp,
                                                    int n, int s, const LmDeviceState* st, int gate_running) {
+  pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
   const int pair = blockIdx.z >> 1, tri = blockIdx.z & 1;
   const int b1 = 2 * pair * s, b2 = b1 + s;
@@ -183,6 +185,7 @@ constexpr int kTmvRows = 64, kTmvCols = 128;
 template <class T, bool LOWER>
 __global__ void __launch_bounds__(256) k_tri_mv(const T* __restrict__ Inv, int n, const T* __restrict__ x,
                                                 T* __restrict__ part, const LmDeviceState* st, int gate_running) {
+  pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
   __shared__ T red[4][kTmvRows];
   const int r0 = blockIdx.x * kTmvRows, c0 = blockIdx.y * kTmvCols;
@@ -215,6 +218,7 @@ __global__ void __launch_bounds__(256) k_tri_mv(const T* __restrict__ Inv, int n
 template <class T, bool LOWER>
 __global__ void k_tri_mv_sum(const T* __restrict__ part, int nslices, int n, const T* __restrict__ x, T* __restrict__ y,
                              const LmDeviceState* st, int gate_running) {
+  pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;

@@ -42,9 +42,12 @@ def _run(env_extra):
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 
-def test_forced_nccl_path_matches_single_rank(engine_lib):
-    plain = _run({"CPF_FORCE_NCCL": "0"})
-    nccl = _run({"CPF_FORCE_NCCL": "1"})
+@pytest.mark.parametrize("oz", ["0", "1"])
+def test_forced_nccl_path_matches_single_rank(engine_lib, oz):
+    # oz=1: the int8 Ozaki tensor passes (forced for every real case) under the multi-rank path --
+    # config 4's default at scale (allreduce of their M_1/Z partials, allgather of M_N rows)
+    plain = _run({"CPF_FORCE_NCCL": "0", "CPF_OZ": oz})
+    nccl = _run({"CPF_FORCE_NCCL": "1", "CPF_OZ": oz})
     for name in plain:
         assert plain[name]["seq"] == nccl[name]["seq"]
         np.testing.assert_allclose(nccl[name]["err"], plain[name]["err"], rtol=0, atol=1e-13)
