@@ -41,6 +41,7 @@ extern "C" {
 #define CPF_E_ZERODIV (-6)     /* ZeroDivisionError: zero tensor / zero-norm component (solver.py:323-324, kruskal.py:184-185) */
 #define CPF_E_UNSUPPORTED (-7) /* shape outside the engine's envelope (order > 8, NR^2 too large, ...) */
 #define CPF_E_STATE (-8)       /* call out of order (no tensor / factors bound) */
+#define CPF_E_FORMAT (-9)      /* cptn.FormatError(ValueError): malformed tensor file (cptn.py:24-59) */
 
 /* scalar kinds */
 #define CPF_REAL 0     /* float64 */
@@ -107,6 +108,14 @@ void* cpf_engine_stream(cpf_engine* e);
 /* Bind the local slab (column-major, prod(dims[0:N-1]) * (hi-lo) elements).
  * where = 0: host memory, copied (pinned or pageable); where = 1: device memory, borrowed. */
 int cpf_engine_set_tensor(cpf_engine* e, const void* data, int64_t nelem, int where);
+/* Stream this engine's slab of a CPTN tensor file (cptn.py:1-7 layout: 16-byte header, N x u64
+ * dims, then the scalars column-major) straight into device memory: the slab of the last mode is
+ * one contiguous byte range of the payload, read with pread into two pinned staging buffers and
+ * copied asynchronously -- no host copy of the tensor.  Replaces cptn.read_tensor (cptn.py:37-59)
+ * + DenseTensor upload on the fit path (cli.py:115-118).  `payload_offset` = header + dims bytes
+ * (the caller validated magic / version / kind / dims); a payload whose size is not the dims'
+ * product fails with CPF_E_FORMAT and the reference's message. */
+int cpf_engine_load_cptn(cpf_engine* e, const char* path, int64_t payload_offset);
 /* Factors, stacked (kruskal.py:70-72).  Host memory; full (replicated) factors on every rank. */
 int cpf_engine_set_factors(cpf_engine* e, const void* stacked);
 int cpf_engine_get_factors(cpf_engine* e, void* stacked);

@@ -17,6 +17,7 @@ from .solver import (
     SingularKernelError,
     fit,
     fit_complex,
+    fit_file,
     flm_step,
     mttkrp,
     random_init,
@@ -29,6 +30,6 @@ __version__ = "0.1.0"
 __all__ = [
     "COMPLEX", "REAL", "DenseTensor", "KruskalModel", "ScalarKindError", "model_from_vector",
     "LM_VARIANTS", "MU_OVERFLOW", "VARIANTS", "FitConfig", "FitResult", "IterRecord",
-    "SingularKernelError", "fit", "fit_complex", "flm_step", "mttkrp", "random_init",
+    "SingularKernelError", "fit", "fit_complex", "fit_file", "flm_step", "mttkrp", "random_init",
     "relative_error", "slab_bounds",
 ]

@@ -27,6 +27,7 @@ CPF_E_NCCL = -5
 CPF_E_ZERODIV = -6
 CPF_E_UNSUPPORTED = -7
 CPF_E_STATE = -8
+CPF_E_FORMAT = -9
 
 CPF_REAL = 0
 CPF_COMPLEX = 1
@@ -83,6 +84,7 @@ EXPORTED_SYMBOLS = (
     "cpf_engine_launch_count",
     "cpf_engine_unfolding_gram",
     "cpf_engine_pass_impl",
+    "cpf_engine_load_cptn",
 )
 
 
@@ -130,6 +132,7 @@ def _declare(lib) -> None:
         "cpf_engine_launch_count": (I64, [P]),
         "cpf_engine_unfolding_gram": (I, [P, I, P]),
         "cpf_engine_pass_impl": (I, [P]),
+        "cpf_engine_load_cptn": (I, [P, ctypes.c_char_p, I64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -178,6 +181,10 @@ def _raise_for(rc: int, msg: str):
         raise TypeError(msg)
     if rc == CPF_E_ZERODIV:
         raise ZeroDivisionError(msg)
+    if rc == CPF_E_FORMAT:
+        from .cptn import FormatError
+
+        raise FormatError(msg)
     if rc == CPF_E_UNSUPPORTED:
         raise ValueError(f"not supported on the B200 backend: {msg}")
     raise NativeError(f"native engine error {rc}: {msg}")
@@ -240,6 +247,9 @@ class Engine:
         flat = np.ravel(arr, order="F")  # no copy for a Fortran-contiguous slab
         self._keep = flat
         self._check(self._lib.cpf_engine_set_tensor(self._h, flat.ctypes.data, flat.size, 0))
+
+    def load_cptn(self, path, payload_offset: int):
+        self._check(self._lib.cpf_engine_load_cptn(self._h, str(path).encode(), int(payload_offset)))
 
     def set_tensor_device(self, ptr: int, nelem: int):
         self._check(self._lib.cpf_engine_set_tensor(self._h, ctypes.c_void_p(ptr), int(nelem), 1))

@@ -7,6 +7,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -63,6 +67,7 @@ struct EngineBase {
   virtual void slab(int64_t* lo, int64_t* hi) const = 0;
   virtual void* stream() = 0;
   virtual void set_tensor(const void* p, int64_t n, int where) = 0;
+  virtual void load_cptn(const char* path, int64_t payload_offset) = 0;
   virtual void set_factors(const void* p) = 0;
   virtual void get_factors(void* p) = 0;
   virtual void fit_begin(int variant, double tau, double tol, int max_iters, cpf_status* st) = 0;
@@ -1318,6 +1323,58 @@ struct Engine final : EngineBase {
     oz_split();
     have_tensor = true;
   }
+  // CPTN file -> this rank's slab in device memory, double-buffered through pinned staging
+  void load_cptn(const char* path, int64_t payload_off) override {
+    CPF_CUDA_CHECK(cudaSetDevice(dev));
+    if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) throw ApiError(CPF_E_ARG, std::string("cannot open ") + path);
+    struct FdGuard { int fd; ~FdGuard() { ::close(fd); } } guard{fd};
+    struct stat sb;
+    if (fstat(fd, &sb) != 0) throw ApiError(CPF_E_ARG, std::string("cannot stat ") + path);
+    const int64_t es = (int64_t)sizeof(T);
+    const int64_t count = Lrows * IN;
+    const int64_t have = ((int64_t)sb.st_size - payload_off) / es;
+    if ((int64_t)sb.st_size < payload_off || have != count || ((int64_t)sb.st_size - payload_off) % es != 0)
+      throw ApiError(CPF_E_FORMAT, "expected " + std::to_string(count) + " scalars, found " + std::to_string(have));
+    posix_fadvise(fd, 0, 0, POSIX_FADV_SEQUENTIAL);
+    if (!Yown) {
+      void* q = nullptr;
+      CPF_CUDA_CHECK(cudaMalloc(&q, std::max<int64_t>(Jloc, 1) * sizeof(T)));
+      Yown = static_cast<T*>(q);
+    }
+    const int64_t bytes = Jloc * es;
+    const int64_t start = payload_off + slab_lo * Lrows * es;
+    const int64_t chunk = std::min<int64_t>(bytes, (int64_t)64 << 20);
+    void* stage[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    struct Staging {
+      void** b; cudaEvent_t* e;
+      ~Staging() { for (int i = 0; i < 2; ++i) { if (b[i]) cudaFreeHost(b[i]); if (e[i]) cudaEventDestroy(e[i]); } }
+    } sg{stage, done};
+    for (int i = 0; i < 2 && chunk > 0; ++i) {
+      CPF_CUDA_CHECK(cudaMallocHost(&stage[i], (size_t)chunk));
+      CPF_CUDA_CHECK(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    }
+    int k = 0;
+    for (int64_t off = 0; off < bytes; off += chunk, ++k) {
+      const int b = k & 1;
+      const int64_t n = std::min(chunk, bytes - off);
+      if (k >= 2) CPF_CUDA_CHECK(cudaEventSynchronize(done[b]));  // staging buffer free again
+      int64_t got = 0;
+      while (got < n) {
+        const ssize_t r = ::pread(fd, static_cast<char*>(stage[b]) + got, (size_t)(n - got), (off_t)(start + off + got));
+        if (r <= 0) throw ApiError(CPF_E_FORMAT, std::string("short read in ") + path);
+        got += r;
+      }
+      CPF_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<char*>(Yown) + off, stage[b], (size_t)n, cudaMemcpyHostToDevice, s));
+      CPF_CUDA_CHECK(cudaEventRecord(done[b], s));
+    }
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    Y = Yown;
+    oz_split();
+    have_tensor = true;
+  }
   void set_factors(const void* p) override {
     CPF_CUDA_CHECK(cudaMemcpyAsync(A, p, RT * sizeof(T), cudaMemcpyHostToDevice, s));
     have_factors = true;
@@ -1686,6 +1743,11 @@ void* cpf_engine_stream(cpf_engine* e) { return (e && e->impl) ? e->impl->stream
 int cpf_engine_set_tensor(cpf_engine* e, const void* data, int64_t nelem, int where) {
   if (!e || !e->impl) return CPF_E_STATE;
   return guarded(e, [&] { e->impl->set_tensor(data, nelem, where); });
+}
+
+int cpf_engine_load_cptn(cpf_engine* e, const char* path, int64_t payload_offset) {
+  if (!e || !e->impl || !path) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->load_cptn(path, payload_offset); });
 }
 
 int cpf_engine_set_factors(cpf_engine* e, const void* stacked) {

@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native
-from .tensor import COMPLEX, DenseTensor, KruskalModel, as_dense, as_model, model_from_vector, require_same_kind
+from .tensor import COMPLEX, REAL, DenseTensor, KruskalModel, as_dense, as_model, model_from_vector, require_same_kind
 
 VARIANTS = ("flm-a", "flm-b", "auto", "als", "als-ls", "dgn-oracle")   # solver.py:44
 LM_VARIANTS = ("flm-a", "flm-b", "auto")
@@ -206,27 +206,18 @@ def _make_engine(y: DenseTensor, rank: int, device, distributed, slab_of=None):
     return eng
 
 
-def fit(y, config: FitConfig, *, device=None, distributed=None, slab_of=None) -> FitResult:
-    """Decompose ``y`` with the fLM damped Gauss-Newton loop (solver.py:278-291, 319-384).
-
-    ``distributed``: None (single GPU), True (default torch.distributed group) or a process group;
-    the tensor is then slab-sharded along its last mode across the group's ranks, every rank
-    returns the same result.  ``slab_of``: when given (the global size of the last mode), ``y``
-    holds only this rank's slab of the last mode (``slab_bounds``), so no rank needs the whole
-    tensor in host memory.
-    """
-    t0 = time.monotonic()
+def _check_lm(config: FitConfig):
     if config.variant not in LM_VARIANTS:
         raise ValueError(f"variant {config.variant!r} is not supported on the B200 backend "
                          "(only the fast damped Gauss-Newton variants 'auto', 'flm-a', 'flm-b')")
-    y = as_dense(y)
-    gdims = y.dims if slab_of is None else tuple(y.dims[:-1]) + (int(slab_of),)
-    rng = np.random.default_rng([config.seed, 0])
     if config.init not in ("svd", "random"):
         raise ValueError(f"unknown init {config.init!r}")
-    eng = _make_engine(y, config.rank, device, distributed, slab_of)
+
+
+def _run_fit(eng, gdims, scalar_kind: str, config: FitConfig, rng) -> FitResult:
+    """The LM loop on an engine whose tensor is bound (solver.py:319-384); closes the engine."""
     try:
-        init = _init_model(_Dims(gdims, y.scalar_kind), config, rng, eng)
+        init = _init_model(_Dims(gdims, scalar_kind), config, rng, eng)
         eng.set_factors(init.as_vector())
         st = eng.fit_begin(config.variant, config.tau, config.tol, config.max_iters)
         while st.stopped == _native.STOP_RUNNING:
@@ -239,6 +230,58 @@ def fit(y, config: FitConfig, *, device=None, distributed=None, slab_of=None) ->
             raise ZeroDivisionError("a component of the accepted candidate has a zero-norm vector")
     finally:
         eng.close()
+    return result
+
+
+def fit(y, config: FitConfig, *, device=None, distributed=None, slab_of=None) -> FitResult:
+    """Decompose ``y`` with the fLM damped Gauss-Newton loop (solver.py:278-291, 319-384).
+
+    ``distributed``: None (single GPU), True (default torch.distributed group) or a process group;
+    the tensor is then slab-sharded along its last mode across the group's ranks, every rank
+    returns the same result.  ``slab_of``: when given (the global size of the last mode), ``y``
+    holds only this rank's slab of the last mode (``slab_bounds``), so no rank needs the whole
+    tensor in host memory.
+    """
+    t0 = time.monotonic()
+    _check_lm(config)
+    y = as_dense(y)
+    gdims = y.dims if slab_of is None else tuple(y.dims[:-1]) + (int(slab_of),)
+    rng = np.random.default_rng([config.seed, 0])
+    eng = _make_engine(y, config.rank, device, distributed, slab_of)
+    result = _run_fit(eng, gdims, y.scalar_kind, config, rng)
+    result.time_ms = (time.monotonic() - t0) * 1e3
+    return result
+
+
+def fit_file(path, config: FitConfig, *, device=None, distributed=None, complex_only: bool = False) -> FitResult:
+    """``fit`` of a CPTN tensor file (cli.py:115-118 reads it with cptn.read_tensor first): the
+    engine streams its slab of the file straight into device memory (``cpf_engine_load_cptn``),
+    so neither the whole tensor nor a host copy of it is ever materialised.  Same result, errors
+    and ``time_ms`` convention as ``fit`` (the file read is inside the timed region)."""
+    from . import cptn
+
+    t0 = time.monotonic()
+    _check_lm(config)
+    h = cptn.read_header(path)
+    if len(h.dims) < 2:
+        raise ValueError("the fLM solver needs a tensor of order >= 2")
+    if complex_only and h.kind != 1:
+        raise TypeError("expected a complex tensor")
+    kind = _native.CPF_COMPLEX if h.kind else _native.CPF_REAL
+    dev = 0 if device is None else int(device)
+    if distributed is not None:
+        ctx = distributed if isinstance(distributed, _Dist) else _Dist(distributed if distributed is not True else None)
+        uid = ctx.unique_id() if ctx.world > 1 else None
+        eng = _native.Engine(kind, h.dims, config.rank, dev, ctx.rank, ctx.world, uid)
+    else:
+        eng = _native.Engine(kind, h.dims, config.rank, dev)
+    try:
+        cptn.load_to_engine(eng, path, h)
+    except BaseException:
+        eng.close()
+        raise
+    rng = np.random.default_rng([config.seed, 0])
+    result = _run_fit(eng, h.dims, COMPLEX if h.kind else REAL, config, rng)
     result.time_ms = (time.monotonic() - t0) * 1e3
     return result
 
