@@ -29,9 +29,15 @@ def sources():
 STAMP = OUT.with_suffix(".srchash")
 
 
+def _extra_defs() -> list:
+    """Diagnostic -D flags (CPF_NVCC_DEFS="-DCPF_PANEL_TIMING ..."); part of the build hash."""
+    return os.environ.get("CPF_NVCC_DEFS", "").split()
+
+
 def source_hash() -> str:
     """Content hash of every source the library is built from (mtimes do not survive snapshots)."""
     h = hashlib.sha256()
+    h.update(" ".join(_extra_defs()).encode())
     for p in sources():
         h.update(p.name.encode())
         h.update(p.read_bytes())
@@ -52,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     tmp = OUT.with_suffix(".so.tmp")
     cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
            "-Xptxas", "-warn-spills" if not verbose else "-v",
-           "-o", str(tmp), str(CSRC / "engine.cu"), "-lnccl"]
+           *_extra_defs(), "-o", str(tmp), str(CSRC / "engine.cu"), "-lnccl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

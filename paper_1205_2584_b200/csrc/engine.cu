@@ -172,6 +172,28 @@ struct Engine final : EngineBase {
 
   // profiling
   bool prof = false;
+  // diagnostic section marks on stream s in profiled (eager) iterations (CPF_MARKS=1 prints the
+  // per-section totals from phase_times): 0 candidate, 1 normalise + pass A + trial fit + decide,
+  // 2 commit, 3 fork (pass B || next core system) to join
+  std::vector<std::pair<int, cudaEvent_t>> marks;
+  double mark_ms[4] = {0, 0, 0, 0};
+  // CPF_MARKS=3: the marks are external event-record nodes of the captured iteration graph, read
+  // after every replay (graph-mode section times; diagnostic, one replay per poll)
+  const bool gmarks = [] { const char* e = getenv("CPF_MARKS"); return e && e[0] == '3'; }();
+  cudaEvent_t gmark[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool capturing = false;
+  void mark(int id) {
+    if (gmarks && capturing) {
+      if (!gmark[id]) CPF_CUDA_CHECK(cudaEventCreate(&gmark[id]));
+      CPF_CUDA_CHECK(cudaEventRecordWithFlags(gmark[id], s, cudaEventRecordExternal));
+      return;
+    }
+    if (!prof) return;
+    cudaEvent_t e;
+    CPF_CUDA_CHECK(cudaEventCreate(&e));
+    CPF_CUDA_CHECK(cudaEventRecord(e, s));
+    marks.push_back({id, e});
+  }
   struct Ev { int ph; cudaEvent_t a, b; };
   std::vector<Ev> evs;
   double ph_ms[kNumPhases] = {0};
@@ -1190,8 +1212,11 @@ struct Engine final : EngineBase {
            (const DevFlags*)fl, gate, (const int*)kinv_ok, (const double*)nullptr);
     launch(k_phi_assemble<T>, nblocks((int64_t)nB * nB, 256), 256, 0, Phi, N, R, (const T*)Cg, (const T*)Gi,
            (const T*)Gp, (const T*)Gf, (const LmDeviceState*)st, gr);
+    mark(5);
     lu_factor(gr);
+    mark(6);
     if (use_inv) tri_invert(gr);
+    mark(7);
   }
 
   void candidate(int refine_steps, int gate, bool core_ready = false) {
@@ -1461,7 +1486,9 @@ struct Engine final : EngineBase {
   void iteration() {
     const int g = kRunning;
     pdl_now = true;
+    mark(0);
     candidate(2, g, /*core_ready=*/true);  // Phi(mu_t, cache_t) was factored at the end of t-1
+    mark(1);
     // delta' = cand - model (solver.py:348)
     axpby(Cand, 1.0, A, -1.0, V1, g);
     // normalised candidate: trial fit and, if accepted, the new model (solver.py:362)
@@ -1477,6 +1504,7 @@ struct Engine final : EngineBase {
     direct_resid(Ac, dscal + 4, kOnDirect);
     direct_resid(A, dscal + 5, kOnCurDirect);
     launch(k_decide, 1, 1, 0, st, fl, dtrace, (const double*)dscal);
+    mark(2);
     // commit an accepted candidate (solver.py:361-367): model, cache, MTTKRPs, gradient
     const int ga = kOnAccept;
     launch(k_copy<T>, nblocks(RT, 256), 256, 0, (const T*)Ac, A, RT, (const LmDeviceState*)st, (const DevFlags*)fl, ga);
@@ -1488,6 +1516,7 @@ struct Engine final : EngineBase {
     // fork: pass B (M_N of the new model) + gradient on s3, while s factors the next step's
     // core system Phi(mu_{t+1}, cache_{t+1}) -- independent of Y, so the two overlap
     pdl_now = false;
+    mark(3);
     if (serial) {  // diagnostic (CPF_SERIAL=1): no overlap, phases time standalone
       pass_b(A, M, ga);
       gradient(ga);
@@ -1504,6 +1533,7 @@ struct Engine final : EngineBase {
       CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evG, 0));
     }
     launch(k_clear_pending, 1, 1, 0, fl);
+    mark(4);
   }
 
   void capture_iteration() {
@@ -1511,8 +1541,11 @@ struct Engine final : EngineBase {
     const int64_t before = nlaunch;
     CPF_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     try {
+      capturing = true;
       iteration();
+      capturing = false;
     } catch (...) {
+      capturing = false;
       cudaStreamEndCapture(s, &g);
       if (g) cudaGraphDestroy(g);
       throw;
@@ -1531,7 +1564,7 @@ struct Engine final : EngineBase {
     if (use_graph && !gexec) capture_iteration();
     int k = 0;
     while (k < n && hst->stopped == 0) {
-      const int batch = use_graph ? std::min(kPoll, n - k) : 1;
+      const int batch = use_graph && !gmarks ? std::min(kPoll, n - k) : 1;
       for (int b = 0; b < batch; ++b) {
         if (use_graph) {
           CPF_CUDA_CHECK(cudaGraphLaunch(gexec, s));
@@ -1542,6 +1575,19 @@ struct Engine final : EngineBase {
       }
       k += batch;
       pull_state();
+      if (use_graph && gmarks && gmark[0] && gmark[4]) {
+        float t[4];
+        for (int i = 0; i < 4; ++i) CPF_CUDA_CHECK(cudaEventElapsedTime(&t[i], gmark[i], gmark[i + 1]));
+        fprintf(stderr, "[cpf graph iter] %.3f %.3f %.3f %.3f", t[0], t[1], t[2], t[3]);
+        if (gmark[5] && gmark[6] && gmark[7]) {  // inside the fork: core prep | LU | inverse (from mark 3)
+          float u[3];
+          CPF_CUDA_CHECK(cudaEventElapsedTime(&u[0], gmark[3], gmark[5]));
+          CPF_CUDA_CHECK(cudaEventElapsedTime(&u[1], gmark[5], gmark[6]));
+          CPF_CUDA_CHECK(cudaEventElapsedTime(&u[2], gmark[6], gmark[7]));
+          fprintf(stderr, "  | core prep %.3f LU %.3f inverse %.3f", u[0], u[1], u[2]);
+        }
+        fprintf(stderr, "\n");
+      }
     }
     fill_status(o);
   }
@@ -1610,6 +1656,22 @@ struct Engine final : EngineBase {
       cudaEventDestroy(e.b);
     }
     evs.clear();
+    const bool verbose = getenv("CPF_MARKS") && getenv("CPF_MARKS")[0] == '2';
+    for (size_t i = 0; i + 1 < marks.size(); ++i) {
+      const int a = marks[i].first, b = marks[i + 1].first;
+      if (b == a + 1 && a < 4) {
+        float t = 0.f;
+        CPF_CUDA_CHECK(cudaEventElapsedTime(&t, marks[i].second, marks[i + 1].second));
+        mark_ms[a] += t;
+        if (verbose) fprintf(stderr, "%s%.3f%s", a == 0 ? "[cpf iter] " : " ", t, a == 3 ? "\n" : "");
+      }
+    }
+    for (auto& m : marks) cudaEventDestroy(m.second);
+    marks.clear();
+    if (const char* e = getenv("CPF_MARKS"))
+      if (e[0] == '1')
+        fprintf(stderr, "[cpf marks] candidate %.3f  passA+decide %.3f  commit %.3f  fork %.3f ms (totals)\n",
+                mark_ms[0], mark_ms[1], mark_ms[2], mark_ms[3]);
     for (int i = 0; i < n && i < kNumPhases; ++i) {
       ms[i] = ph_ms[i];
       cnt[i] = ph_cnt[i];
@@ -1810,6 +1872,22 @@ int cpf_engine_unfolding_gram(cpf_engine* e, int mode, void* out) {
 
 }  // extern "C"
 
-extern "C" int cpf_debug_panel_cycles(long long* out8) {
-  return cudaMemcpyFromSymbol(out8, cpf::g_panel_cycles, sizeof(long long) * 8) == cudaSuccess ? 0 : -4;
+// diagnostic: on != 0 resets and enables the LU timeline, on == 0 disables it and copies it out
+extern "C" int cpf_debug_lu_trace(int on, unsigned long long* out) {
+  static unsigned long long init[3 * 512 * 2];
+  if (on) {
+    for (int i = 0; i < 3 * 512; ++i) { init[2 * i] = ~0ull; init[2 * i + 1] = 0ull; }
+    if (cudaMemcpyToSymbol(cpf::g_lu_trace, init, sizeof(init)) != cudaSuccess) return -4;
+  } else if (out) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return -4;
+    if (cudaMemcpyFromSymbol(out, cpf::g_lu_trace, sizeof(init)) != cudaSuccess) return -4;
+    if (cudaMemcpyFromSymbol(out + 3 * 512 * 2, cpf::g_lu_clk, sizeof(unsigned long long) * 1024) != cudaSuccess)
+      return -4;
+  }
+  return cudaMemcpyToSymbol(cpf::g_lu_trace_on, &on, sizeof(int)) == cudaSuccess ? 0 : -4;
+}
+
+extern "C" int cpf_debug_panel_cycles(long long* out12) {
+  if (cudaMemcpyFromSymbol(out12 + 8, cpf::g_panel_seg, sizeof(long long) * 8) != cudaSuccess) return -4;
+  return cudaMemcpyFromSymbol(out12, cpf::g_panel_cycles, sizeof(long long) * 8) == cudaSuccess ? 0 : -4;
 }

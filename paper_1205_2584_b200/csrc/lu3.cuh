@@ -20,6 +20,30 @@ namespace cpf {
 
 // per-phase cycle counters of the panel kernel (CTA 0, thread 0), enabled with -DCPF_PANEL_TIMING
 __device__ long long g_panel_cycles[8];
+__device__ long long g_panel_seg[12];
+#ifdef CPF_PANEL_TIMING
+#define PSEG(i, t0) do { if (threadIdx.x == 0 && blockIdx.x == 0) { const long long tn = clock64(); atomicAdd((unsigned long long*)&g_panel_seg[i], (unsigned long long)(tn - t0)); t0 = tn; } } while (0)
+#else
+#define PSEG(i, t0) do {} while (0)
+#endif  // lu4 panel (CTA 0): load+sync, column loop, write-back+sync, total
+
+// Diagnostic LU timeline (cpf_debug_lu_trace): per (kind, step) the first start and last end
+// %globaltimer of the panel (kind 0), U12 (1) and trailing-GEMM (2) launches of one iteration.
+__device__ int g_lu_trace_on;
+__device__ unsigned long long g_lu_trace[3 * 512 * 2];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ unsigned long long g_lu_clk[512 * 2];  // panel CTA 0: clock64 at start / end (SM clock)
+__device__ __forceinline__ void lu_trace(int kind, int step, int end) {
+  if (!g_lu_trace_on || threadIdx.x != 0 || step < 0 || step >= 512) return;
+  unsigned long long* e = g_lu_trace + 2 * (kind * 512 + step);
+  if (end) atomicMax(e + 1, gtimer());
+  else atomicMin(e, gtimer());
+  if (kind == 0 && blockIdx.x == 0) g_lu_clk[2 * step + end] = (unsigned long long)clock64();
+}
 
 template <class T>
 __device__ __forceinline__ T shfl_val(T v, int src);
@@ -92,7 +116,7 @@ struct PanelPrev {
 template <class T, int RPT, int NTHR>
 __device__ __forceinline__ void panel_load(T (&a)[RPT][kLuMaxKB], const T* __restrict__ A, int lda, int k0, int kb,
                                            const int (&myrow)[RPT], const bool (&alive)[RPT], const PanelPrev<T>& pv,
-                                           int* gl, T* u12, T* stage = nullptr) {
+                                           int* gl, T* u12, T* stage = nullptr, T* linv = nullptr) {
   constexpr int KB = kLuMaxKB;
   const int tid = threadIdx.x;
   if (pv.kp0 < 0) {
@@ -104,8 +128,13 @@ __device__ __forceinline__ void panel_load(T (&a)[RPT][kLuMaxKB], const T* __res
     }
     return;
   }
+#ifdef CPF_PANEL_TIMING
+  long long pt0 = clock64();
+#endif
   const int G = *pv.gcount;
   for (int e = tid; e < 2 * G; e += NTHR) gl[e] = pv.gather[e];
+  if (linv)
+    for (int e = tid; e < KB * KB; e += NTHR) linv[e] = pv.invL[e];
   __syncthreads();
   auto src_of = [&](int r) {
     int s = r;
@@ -113,14 +142,21 @@ __device__ __forceinline__ void panel_load(T (&a)[RPT][kLuMaxKB], const T* __res
       if (gl[2 * g] == r) s = gl[2 * g + 1];
     return s;
   };
-  // A12 (the step's top rows of this block, interchanged) -> u12[i][q]
-  for (int e = tid; e < KB * KB; e += NTHR) {
-    const int i = e % KB, q = e / KB;
-    T v = zero_of<T>();
-    if (i < pv.kbp && q < kb) v = A[(int64_t)src_of(pv.kp0 + i) + (int64_t)lda * (k0 + q)];
-    u12[i * KB + q] = v;
+  // A12 (the step's top rows of this block, interchanged) -> u12[i][q]; NTHR % KB == 0, so a
+  // thread's elements share one row i and one gather lookup
+  static_assert(NTHR % KB == 0, "panel threads");
+  {
+    const int i = tid % KB;
+    const int64_t srow = i < pv.kbp ? src_of(pv.kp0 + i) : 0;
+    for (int e = tid; e < KB * KB; e += NTHR) {
+      const int q = e / KB;
+      T v = zero_of<T>();
+      if (i < pv.kbp && q < kb) v = A[srow + (int64_t)lda * (k0 + q)];
+      u12[i * KB + q] = v;
+    }
   }
   __syncthreads();
+  PSEG(4, pt0);
   // U12 = inv(L11) A12 (same summation order as k_u12)
   T uv[(KB * KB + NTHR - 1) / NTHR];
 #pragma unroll
@@ -129,7 +165,13 @@ __device__ __forceinline__ void panel_load(T (&a)[RPT][kLuMaxKB], const T* __res
     T acc = zero_of<T>();
     if (e < KB * KB) {
       const int i = e / KB, q = e % KB;
-      for (int p = 0; p <= i; ++p) fma_acc(acc, pv.invL[i + KB * p], u12[p * KB + q]);
+      if (linv) {
+#pragma unroll
+        for (int p = 0; p < KB; ++p)
+          if (p <= i) fma_acc(acc, linv[i + KB * p], u12[p * KB + q]);
+      } else {
+        for (int p = 0; p <= i; ++p) fma_acc(acc, pv.invL[i + KB * p], u12[p * KB + q]);
+      }
     }
     uv[t] = acc;
   }
@@ -140,40 +182,49 @@ __device__ __forceinline__ void panel_load(T (&a)[RPT][kLuMaxKB], const T* __res
     if (e < KB * KB) u12[e] = uv[t];
   }
   __syncthreads();
+  PSEG(5, pt0);
   // this panel's rows: interchanged block row minus L21 U12.  With a stage (the caller's
-  // per-thread smem slots, stride RPT*NTHR) one row is live at a time and the frame is loaded
-  // afterwards, so the update does not add to the column loop's register pressure.
+  // per-thread smem slots, stride RPT*NTHR) the frame is loaded afterwards, so the update does not
+  // add to the column loop's register pressure.  All RPT rows are updated together: each U12 value
+  // read from shared memory serves every row of the thread.
+  {
+    T v[RPT][KB];
+    const T* lrow[RPT];
 #pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    T v[KB];
-    if (!alive[j]) {
-#pragma unroll
-      for (int q = 0; q < KB; ++q) v[q] = zero_of<T>();
-    } else {
+    for (int j = 0; j < RPT; ++j) {
       const int r = k0 + myrow[j];
-      const T* src = A + (int64_t)src_of(r) + (int64_t)lda * k0;
+      const T* src = A + (int64_t)(alive[j] ? src_of(r) : 0) + (int64_t)lda * k0;
 #pragma unroll
-      for (int q = 0; q < KB; ++q) v[q] = q < kb ? src[(int64_t)lda * q] : zero_of<T>();
-      const T* lrow = A + (int64_t)r + (int64_t)lda * pv.kp0;
+      for (int q = 0; q < KB; ++q) v[j][q] = (alive[j] && q < kb) ? src[(int64_t)lda * q] : zero_of<T>();
+      lrow[j] = A + (int64_t)(alive[j] ? r : 0) + (int64_t)lda * pv.kp0;
+    }
 #pragma unroll 1
-      for (int p0 = 0; p0 < pv.kbp; p0 += 8) {
-        T l[8];
+    for (int p0 = 0; p0 < pv.kbp; p0 += 8) {
+      T l[RPT][8];
 #pragma unroll
-        for (int p = 0; p < 8; ++p) l[p] = (p0 + p < pv.kbp) ? lrow[(int64_t)lda * (p0 + p)] : zero_of<T>();
+      for (int j = 0; j < RPT; ++j)
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          const T* ur = u12 + (p0 + p) * KB;
+        for (int p = 0; p < 8; ++p) l[j][p] = (alive[j] && p0 + p < pv.kbp) ? lrow[j][(int64_t)lda * (p0 + p)] : zero_of<T>();
 #pragma unroll
-          for (int q = 0; q < KB; ++q) fms_acc(v[q], l[p], ur[q]);
+      for (int p = 0; p < 8; ++p) {
+        const T* ur = u12 + (p0 + p) * KB;
+#pragma unroll
+        for (int q = 0; q < KB; ++q) {
+          const T u = ur[q];
+#pragma unroll
+          for (int j = 0; j < RPT; ++j) fms_acc(v[j][q], l[j][p], u);
         }
       }
     }
 #pragma unroll
-    for (int q = 0; q < KB; ++q) {
-      if (stage) stage[(size_t)q * RPT * NTHR + j * NTHR + tid] = v[q];
-      else a[j][q] = v[q];
-    }
+    for (int j = 0; j < RPT; ++j)
+#pragma unroll
+      for (int q = 0; q < KB; ++q) {
+        if (stage) stage[(size_t)q * RPT * NTHR + j * NTHR + tid] = v[j][q];
+        else a[j][q] = v[j][q];
+      }
   }
+  PSEG(6, pt0);
   if (stage) {
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
@@ -436,6 +487,7 @@ __global__ void __launch_bounds__(256) k_u12(T* __restrict__ A, int cend, int ld
                                              int cbeg) {
   pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
+  lu_trace(1, k0 / KB, 0);
   __shared__ T Li[KB * KB];
   __shared__ T Bt[KB * 64];
   const int c0 = cbeg + blockIdx.x * 64;
@@ -453,6 +505,7 @@ __global__ void __launch_bounds__(256) k_u12(T* __restrict__ A, int cend, int ld
     for (int j = 0; j <= i; ++j) fma_acc(acc, Li[i + KB * j], Bt[j + c * KB]);
     A[(int64_t)(k0 + i) + (int64_t)lda * (c0 + c)] = acc;
   }
+  lu_trace(1, k0 / KB, 1);
 }
 
 // C -= A B on the fp64 tensor cores.  C: m x nn at (r0, c0); A = L21 at (r0, k0); B = U12 at (k0, c0).
@@ -467,6 +520,7 @@ __global__ void __launch_bounds__(128) k_gemm_dmma(double* __restrict__ M, int l
                                                    int nn, int k, const LmDeviceState* st, int gate_running) {
   pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
+  lu_trace(2, k0 / 32, 0);
   constexpr int TM = 64, TN = 64, KM = 32, PADA = 68, PADB = 68;
   __shared__ double As[KM * PADA];  // As[q][i] (k-major), stride PADA
   __shared__ double Bs[KM * PADB];  // Bs[q][j]
@@ -516,6 +570,7 @@ __global__ void __launch_bounds__(128) k_gemm_dmma(double* __restrict__ M, int l
           *cp -= acc[i][j][h];
         }
       }
+  lu_trace(2, k0 / 32, 1);
 }
 
 }  // namespace cpf

@@ -32,6 +32,8 @@ size_t panel4_smem_bytes(int CL, int nthr, int rpt) {
   size_t b = 16 + 16 * 2 * (size_t)CL * pkc;                     // mbarriers + packets
   b += sizeof(T) * ((size_t)KB * nthr * rpt + NW * KB + (size_t)KB * KB);  // fin + wrow_s + top
   b += sizeof(double) * NW + sizeof(int) * NW + sizeof(int) * 4 * KB;
+  b = (b + 15) & ~(size_t)15;
+  b += sizeof(T) * (size_t)KB * KB;  // inv(L11) of the previous step (fused load)
   return (b + 15) & ~(size_t)15;
 }
 
@@ -41,6 +43,10 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
                                                        PanelPrev<T> pv) {
   pdl_wait();
   if (st && gate_running && (st->stopped || st->err_code)) return;
+  lu_trace(0, k0 / kLuMaxKB, 0);
+#ifdef CPF_PANEL_TIMING
+  const long long seg0 = clock64();
+#endif
   constexpr int KB = kLuMaxKB;  // 32
   constexpr int CH = 8;         // columns per static chunk
   constexpr int NW = NTHR / 32;
@@ -61,6 +67,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
   int* Dl = pivrows + KB;                                               // [KB]
   int* Vl = Dl + KB;                                                    // [KB]
   int* misc = Vl + KB;                                                  // [KB]
+  T* linv_s = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(misc + KB) + 15) & ~(uintptr_t)15);  // [KB][KB]
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int m = n - k0;
@@ -75,13 +82,16 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
     pcol[j] = -1;
   }
   // PanelPrev scratch: gather list in pivrows..misc, U12 in top, rows staged in fin (all used later)
-  panel_load<T, RPT, NTHR>(a, A, lda, k0, kb, myrow, alive, pv, pivrows, top, fin);
+  panel_load<T, RPT, NTHR>(a, A, lda, k0, kb, myrow, alive, pv, pivrows, top, fin, linv_s);
   if (tid == 0) {
     mbar_init(&pbar[0], 1);
     mbar_init(&pbar[1], 1);
     fence_mbar_init();
   }
   cluster.sync();  // remote CTAs may target pbar only once it is initialised
+#ifdef CPF_PANEL_TIMING
+  const long long seg1 = clock64();
+#endif
   if (rank == 0) panel_prev_store<T, NTHR>(A, lda, k0, kb, pv, top);  // every CTA is past its loads
   const uint32_t pk_tx = (uint32_t)(CL * PK::PKC * 16);
   const uint32_t bar0_u32 = smem_u32(&pbar[0]), bar1_u32 = smem_u32(&pbar[1]);
@@ -213,6 +223,11 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
     }
   }
 #ifdef CPF_PANEL_TIMING
+  const long long seg2 = clock64();
+  if (rank == 0 && tid == 0) {
+    atomicAdd((unsigned long long*)&g_panel_seg[0], (unsigned long long)(seg1 - seg0));
+    atomicAdd((unsigned long long*)&g_panel_seg[1], (unsigned long long)(seg2 - seg1));
+  }
   if (rank == 0 && tid == 0)
     for (int i = 0; i < 6; ++i) atomicAdd((unsigned long long*)&g_panel_cycles[i], (unsigned long long)tacc[i]);
   if (rank == 0 && tid == 0) atomicAdd((unsigned long long*)&g_panel_cycles[7], 1ull);
@@ -251,6 +266,9 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
     for (int q = 0; q < kb; ++q) dst[(int64_t)lda * q] = fin[(size_t)q * ROWS + j * NTHR + tid];
   }
   cluster.sync();  // every CTA's rows are in place (global writes ordered at cluster scope)
+#ifdef CPF_PANEL_TIMING
+  if (rank == 0 && tid == 0) atomicAdd((unsigned long long*)&g_panel_seg[2], (unsigned long long)(clock64() - seg2));
+#endif
   if (rank == 0) {
     for (int e = tid; e < KB * KB; e += NTHR) {
       const int r = e / KB, q = e % KB;
@@ -288,6 +306,10 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
       if (lane == 0) *w.gcount = g;
     }
   }
+#ifdef CPF_PANEL_TIMING
+  if (rank == 0 && tid == 0) atomicAdd((unsigned long long*)&g_panel_seg[3], (unsigned long long)(clock64() - seg0));
+#endif
+  lu_trace(0, k0 / kLuMaxKB, 1);
 }
 
 }  // namespace cpf
