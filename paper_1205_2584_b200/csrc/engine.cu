@@ -538,6 +538,12 @@ struct Engine final : EngineBase {
       // pass A streams alone: no L2 hint (measured 3 % faster); pass B runs beside the LU: evict-first
       oa.dbg = 4;
       if (const char* d = getenv("CPF_OZ_DBG")) oa.dbg = ob.dbg = atoi(d);  // experiments
+      // the two digit-plane images (~2 x 8 B per element) must fit next to everything else with
+      // 2 GB to spare; otherwise stay on the fp64 DMMA passes
+      const size_t need = ((size_t)oa.ntiles * oa.nkb + (size_t)ob.ntiles * ob.nkb) * kOzABytes;
+      size_t free_b = 0, total_b = 0;
+      CPF_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+      if (!force && need + ((size_t)2 << 30) + (size_t)Jloc * sizeof(T) > free_b) return;
       ozYA = dalloc<uint8_t>((size_t)oa.ntiles * oa.nkb * kOzABytes);
       ozYB = dalloc<uint8_t>((size_t)ob.ntiles * ob.nkb * kOzABytes);
       ozFrowA = dalloc<int>((size_t)oa.ntiles * kOzM);
