@@ -30,8 +30,8 @@ size_t panel4_smem_bytes(int CL, int nthr, int rpt) {
   const size_t NW = (size_t)nthr / 32;
   const size_t pkc = (size_t)KB * sizeof(T) / 16 + 2;
   size_t b = 16 + 16 * 2 * (size_t)CL * pkc;                     // mbarriers + packets
-  b += sizeof(T) * ((size_t)KB * nthr * rpt + NW * KB + (size_t)KB * KB);  // fin + wrow_s + top
-  b += sizeof(double) * NW + sizeof(int) * NW + sizeof(int) * 4 * KB;
+  b += sizeof(T) * ((size_t)KB * nthr * rpt + 2 * NW * KB + (size_t)KB * KB);  // fin + wrow_s[2] + top
+  b += sizeof(double) * 2 * NW + sizeof(int) * 2 * NW + sizeof(int) * 4 * KB;
   b = (b + 15) & ~(size_t)15;
   b += sizeof(T) * (size_t)KB * KB;  // inv(L11) of the previous step (fused load)
   return (b + 15) & ~(size_t)15;
@@ -59,11 +59,11 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
   uint64_t* pbar = reinterpret_cast<uint64_t*>(smem_raw);               // [2] packet arrivals (by parity)
   double2* cand_pk = reinterpret_cast<double2*>(smem_raw + 16);         // [2][CL][PKC]
   T* fin = reinterpret_cast<T*>(cand_pk + (size_t)2 * CL * PK::PKC);   // [KB][ROWS] finished columns
-  T* wrow_s = fin + (size_t)KB * ROWS;                                  // [NW][KB] warp candidates
-  T* top = wrow_s + (size_t)NW * KB;                                    // [KB][KB] (rank 0: L11 for inv)
-  double* wkey_v = reinterpret_cast<double*>(top + (size_t)KB * KB);    // [NW]
-  int* wkey_r = reinterpret_cast<int*>(wkey_v + NW);                    // [NW]
-  int* pivrows = wkey_r + NW;                                           // [KB]
+  T* wrow_s = fin + (size_t)KB * ROWS;                                  // [2][NW][KB] warp candidates (by parity)
+  T* top = wrow_s + (size_t)2 * NW * KB;                                // [KB][KB] (rank 0: L11 for inv)
+  double* wkey_v = reinterpret_cast<double*>(top + (size_t)KB * KB);    // [2][NW]
+  int* wkey_r = reinterpret_cast<int*>(wkey_v + 2 * NW);                // [2][NW]
+  int* pivrows = wkey_r + 2 * NW;                                       // [KB]
   int* Dl = pivrows + KB;                                               // [KB]
   int* Vl = Dl + KB;                                                    // [KB]
   int* misc = Vl + KB;                                                  // [KB]
@@ -124,9 +124,14 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
       int wrow, wlane;
       warp_argmax_redux(bv, brow, wv, wrow, wlane);
       PT(0);
-      // ---- (b) the warp's best lane stages its frame row; lane 0 posts the warp key
+      // ---- (b) the warp's best lane stages its frame row; lane 0 posts the warp key (buffers by
+      // column parity: a warp staging column jj+2 has passed column jj+1's barrier, so nobody still
+      // reads column jj's buffer)
+      T* wrow_p = wrow_s + (size_t)par * NW * KB;
+      double* wkv_p = wkey_v + par * NW;
+      int* wkr_p = wkey_r + par * NW;
       if (lane == wlane) {
-        T* dst = wrow_s + wid * KB;
+        T* dst = wrow_p + wid * KB;
 #pragma unroll
         for (int q = 0; q < KB; ++q) {
           T sel = a[0][q];
@@ -135,46 +140,60 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
             if (bj == j) sel = a[j][q];
           dst[q] = sel;
         }
-        wkey_v[wid] = wv;
-        wkey_r[wid] = wrow;
+        wkv_p[wid] = wv;
+        wkr_p[wid] = wrow;
       }
       __syncthreads();
       PT(5);
-      // ---- (c) every warp: CTA argmax over the NW warp keys; the CTA's threads push the packet
+      // ---- (c) every warp: CTA argmax over the NW warp keys
+      double cv;
+      int crow, cw;
       {
-        const double kv = lane < NW ? wkey_v[lane] : 0.0;
-        const int kr = lane < NW ? wkey_r[lane] : 0x7fffffff;
-        double cv;
-        int crow, cw;
+        const double kv = lane < NW ? wkv_p[lane] : 0.0;
+        const int kr = lane < NW ? wkr_p[lane] : 0x7fffffff;
         warp_argmax_redux(kv, kr, cv, crow, cw);
-        const double2* src = reinterpret_cast<const double2*>(wrow_s + cw * KB);
+      }
+      double gv;
+      int cr;
+      const double2* wpk;
+      T rcp;
+      if (CL == 1) {
+        // single-CTA panel (m <= RPT*NTHR rows): the CTA's candidate is the pivot; read its staged
+        // row directly, no packet exchange
+        gv = cv;
+        cr = crow;
+        wpk = reinterpret_cast<const double2*>(wrow_p + cw * KB);
+        rcp = cv != 0.0 ? rcp_of(wrow_p[cw * KB + u]) : zero_of<T>();
+        PT(1);
+      } else {
+        // the CTA's threads push its candidate packet into every CTA of the cluster
+        const double2* src = reinterpret_cast<const double2*>(wrow_p + cw * KB);
         const uint32_t slot = smem_u32(cand_pk + (size_t)(par * CL + rank) * PK::PKC);
         for (int si = tid; si < CL * PK::PKC; si += NTHR) {
           const int r = si / PK::PKC, c = si - r * PK::PKC;
           double2 v;
           if (c < PK::DC) v = src[c];
           else if (c == PK::DC) v = make_double2(cv, __longlong_as_double((long long)crow));
-          else v = as_d2(cv != 0.0 ? rcp_of(wrow_s[cw * KB + u]) : zero_of<T>());
+          else v = as_d2(cv != 0.0 ? rcp_of(wrow_p[cw * KB + u]) : zero_of<T>());
           uint32_t raddr, rbar;
           asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(slot + 16u * c), "r"(r));
           asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(par ? bar1_u32 : bar0_u32), "r"(r));
           st_async16(raddr, v.x, v.y, rbar);
         }
+        if (tid == 0) mbar_expect_tx(&pbar[par], pk_tx);
+        PT(1);
+        mbar_wait(&pbar[par], (uint32_t)((jj >> 1) & 1));
+        PT(2);
+        // ---- (d) winner among the CL CTA candidates (identical everywhere)
+        int gl;
+        {
+          double2 kk = make_double2(0.0, __longlong_as_double(0x7fffffffLL));
+          if (lane < CL) kk = cand_pk[(size_t)(par * CL + lane) * PK::PKC + PK::DC];
+          warp_argmax_redux(kk.x, (int)__double_as_longlong(kk.y), gv, cr, gl);
+        }
+        wpk = cand_pk + (size_t)(par * CL + gl) * PK::PKC;
+        rcp = from_d2<T>(wpk[PK::DC + 1]);
       }
-      if (tid == 0) mbar_expect_tx(&pbar[par], pk_tx);
-      PT(1);
-      mbar_wait(&pbar[par], (uint32_t)((jj >> 1) & 1));
-      PT(2);
-      // ---- (d) winner among the CL CTA candidates (identical everywhere)
-      double gv;
-      int cr, gl;
-      {
-        double2 kk = make_double2(0.0, __longlong_as_double(0x7fffffffLL));
-        if (lane < CL) kk = cand_pk[(size_t)(par * CL + lane) * PK::PKC + PK::DC];
-        warp_argmax_redux(kk.x, (int)__double_as_longlong(kk.y), gv, cr, gl);
-      }
-      const double2* wpk = cand_pk + (size_t)(par * CL + gl) * PK::PKC;
-      const T rcp = from_d2<T>(wpk[PK::DC + 1]);
       const bool zero_piv = (gv == 0.0);
       if (tid == 0) pivrows[jj] = k0 + cr;
       if (zero_piv && rank == 0 && tid == 0 && *w.info == 0) *w.info = k0 + jj + 1;
