@@ -11,7 +11,8 @@
 //   level s: for adjacent blocks (b1, b2) of size s
 //     L: inv([L11 0; L21 L22])  -> X21 = -inv(L22) (L21 inv(L11))
 //     U: inv([U11 U12; 0 U22])  -> X12 = -inv(U11) (U12 inv(U22))
-// Products are fp64/complex128 DFMA tiles (64x64 per CTA, 16 K-rows per smem stage).
+// Products are 64x64 tiles per CTA, 16 K-rows per smem stage: fp64 on the DMMA tensor pipe,
+// complex128 as DFMA.
 #pragma once
 #include "cpf_common.cuh"
 
@@ -150,32 +151,77 @@ __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* 
     stash(0);
   }
   __syncthreads();
-  for (int k0 = kbeg; k0 < kend; k0 += KS) {
-    const bool more = k0 + KS < kend;
-    if (more) fetch(k0 + KS);
+  if constexpr (sizeof(T) == 8) {
+    // fp64: the 64x64 tile on the tensor cores (mma.sync m8n8k4.f64 -> DMMA), 8 warps of 32x16:
+    // per 4-deep K step 4 A and 2 B fragments feed 8 DMMAs (the SIMT loop needs 8 LDS per 16 FMA)
+    const int lane = tid & 31, wid = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int wm = (wid & 1) * 32, wn = (wid >> 1) * 16;
+    double dacc[4][2][2];
 #pragma unroll
-    for (int q = 0; q < KS; ++q) {
-      T av[4], bv[4];
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = As[buf][q][tx + 16 * i];
+      for (int j = 0; j < 2; ++j) dacc[i][j][0] = dacc[i][j][1] = 0.0;
+    for (int k0 = kbeg; k0 < kend; k0 += KS) {
+      const bool more = k0 + KS < kend;
+      if (more) fetch(k0 + KS);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = Bs[buf][q][ty + 16 * j];
+      for (int q = 0; q < KS; q += 4) {
+        double af[4], bf[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i) af[i] = As[buf][q + t4][wm + 8 * i + g];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) fma_acc(acc[i][j], av[i], bv[j]);
+        for (int j = 0; j < 2; ++j) bf[j] = Bs[buf][q + t4][wn + 8 * j + g];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(dacc[i][j][0]), "+d"(dacc[i][j][1])
+                         : "d"(af[i]), "d"(bf[j]));
+      }
+      if (more) stash(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
     }
-    if (more) stash(buf ^ 1);
-    __syncthreads();
-    buf ^= 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = tm + wm + 8 * i + g, c = tn + wn + 8 * j + 2 * t4 + h;
+          if (r < m && c < nn) Cm[(int64_t)(rc + r) + (int64_t)n * (cc + c)] = alpha * dacc[i][j][h];
+        }
+    return;
+  } else {
+    for (int k0 = kbeg; k0 < kend; k0 += KS) {
+      const bool more = k0 + KS < kend;
+      if (more) fetch(k0 + KS);
+#pragma unroll
+      for (int q = 0; q < KS; ++q) {
+        T av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = As[buf][q][tx + 16 * i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = Bs[buf][q][ty + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) fma_acc(acc[i][j], av[i], bv[j]);
+      }
+      if (more) stash(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = tm + tx + 16 * i, c = tn + ty + 16 * j;
+        if (r < m && c < nn) Cm[(int64_t)(rc + r) + (int64_t)n * (cc + c)] = scale(acc[i][j], alpha);
+      }
   }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = tm + tx + 16 * i, c = tn + ty + 16 * j;
-      if (r < m && c < nn) Cm[(int64_t)(rc + r) + (int64_t)n * (cc + c)] = scale(acc[i][j], alpha);
-    }
 }
 
 // y = op(Inv) x for the packed triangular inverse: LOWER -> unit-lower inv(L), else inv(U).
