@@ -98,3 +98,46 @@ def test_two_rank_slab_collectives_match_unsharded(dims):
     # both ranks hold bit-identical reduced data (identical decisions on every rank)
     np.testing.assert_array_equal(res[0][4], res[1][4])
     np.testing.assert_array_equal(res[0][5], res[1][5])
+
+
+def _slab_worker(rank, world, port, path, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1205_2584_b200 import cptn, slab_bounds
+
+        h = cptn.read_header(path)
+        lo, hi = slab_bounds(h.dims[-1], world, rank)
+        mine = cptn.read_slab(path, lo, hi, h)  # only this rank's byte range of the file
+        per = -(-h.dims[-1] // world)
+        pad = np.zeros(tuple(h.dims[:-1]) + (per,), dtype=mine.dtype, order="F")
+        pad[..., : hi - lo] = mine
+        flat = torch.from_numpy(np.ascontiguousarray(pad.reshape(-1, order="F")).view(np.float64))
+        got = [torch.zeros_like(flat) for _ in range(world)]
+        dist.all_gather(got, flat)
+        if rank == 0:
+            parts = [g.numpy().view(mine.dtype).reshape(pad.shape, order="F") for g in got]
+            q.put(np.concatenate(parts, axis=-1)[..., : h.dims[-1]])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("complex_", [False, True])
+def test_cptn_slab_byte_ranges_tile_the_file(tmp_path, complex_):
+    """Each rank reads only its slab's byte range of a CPTN file (the cpf_engine_load_cptn
+    arithmetic); gathered, the slabs are the tensor read_tensor returns."""
+    from paper_1205_2584_b200 import cptn
+    from paper_1205_2584_b200.tensor import DenseTensor
+
+    rng = np.random.default_rng(7)
+    y = rng.standard_normal((5, 4, 7))
+    if complex_:
+        y = y + 1j * rng.standard_normal(y.shape)
+    path = tmp_path / "y.cptn"
+    cptn.write_tensor(path, DenseTensor(y))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_slab_worker, args=(2, _free_port(), str(path), q), nprocs=2, join=True, start_method="spawn")
+    full = q.get(timeout=60)
+    assert np.array_equal(full, cptn.read_tensor(path).data)
