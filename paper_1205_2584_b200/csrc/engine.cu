@@ -358,6 +358,9 @@ struct Engine final : EngineBase {
   // the LU) early-scheduled CTAs would park on the SMs left to the LU (measured 162 -> 140 it/s).
   const bool use_pdl = [] { const char* e = getenv("CPF_PDL"); return !(e && e[0] == '0'); }();
   bool pdl_now = false;
+  // programmatic launch of consecutive LU panels (CPF_PDL_PANEL=1; measured no gain at C4 / C1:
+  // the inter-panel gap shrinks from ~4 to ~1 us but the parked next panel slows the running one)
+  const bool pdl_panels = [] { const char* e = getenv("CPF_PDL_PANEL"); return e && e[0] == '1'; }();
   void plan() {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -469,13 +472,16 @@ struct Engine final : EngineBase {
     cfg.blockDim = dim3(kLu4Thr);
     cfg.dynamicSmemBytes = panel4_smem_bytes<T>(cl, kLu4Thr, kLu4Rpt);
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // consecutive panels on stream s: the next panel's launch overlaps this one's tail
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_panels ? 2 : 1;
     CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_panel_lu4<T, kLu4Rpt, kLu4Thr>, Phi, nB, nB, k0, kb, wk, invl,
                                       (const LmDeviceState*)st, gate_running, pv));
     ++nlaunch;
@@ -488,13 +494,15 @@ struct Engine final : EngineBase {
     cfg.blockDim = dim3(THR);
     cfg.dynamicSmemBytes = panel3_smem_bytes<T>(cl, kLuMaxKB, THR);
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_panels ? 2 : 1;
     CPF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_panel_lu3<T, kLuMaxKB, RPTc, THR>, Phi, nB, nB, k0, kb, wk, invl,
                                       (const LmDeviceState*)st, gate_running, pv));
     ++nlaunch;
