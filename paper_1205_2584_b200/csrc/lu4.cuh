@@ -104,6 +104,24 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
 #define PT(i) do {} while (0)
 #endif
 
+  // (a) my best alive row in a frame column, then the warp argmax (ties -> smaller row).  Column
+  // u+1's search runs inside column u's elimination, right after column u+1 itself is updated, so
+  // its reduction latency overlaps the remaining columns' FMAs.
+  auto warp_best = [&](int fc, double& wv, int& wrow, int& wlane, int& bj) {
+    double bv = 0.0;
+    int brow = 0x7fffffff;
+    bj = 0;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      if (!alive[j]) continue;
+      const double v = pivmag(a[j][fc]);
+      if (brow == 0x7fffffff || v > bv) { bv = v; bj = j; brow = myrow[j]; }
+    }
+    warp_argmax_redux(bv, brow, wv, wrow, wlane);
+  };
+  double nwv;
+  int nwrow, nwlane, nbj;
+  warp_best(0, nwv, nwrow, nwlane, nbj);
 #pragma unroll 1
   for (int c8 = 0; c8 < kb; c8 += CH) {
 #pragma unroll
@@ -111,18 +129,8 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
       const int jj = c8 + u;
       if (jj >= kb) break;
       const int par = u & 1;  // == jj & 1 (c8 is a multiple of 8)
-      // ---- (a) my best alive row in frame column u, then warp argmax (ties -> smaller row)
-      double bv = 0.0;
-      int bj = 0, brow = 0x7fffffff;
-#pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        if (!alive[j]) continue;
-        const double v = pivmag(a[j][u]);
-        if (brow == 0x7fffffff || v > bv) { bv = v; bj = j; brow = myrow[j]; }
-      }
-      double wv;
-      int wrow, wlane;
-      warp_argmax_redux(bv, brow, wv, wrow, wlane);
+      const double wv = nwv;
+      const int wrow = nwrow, wlane = nwlane, bj = nbj;
       PT(0);
       // ---- (b) the warp's best lane stages its frame row; lane 0 posts the warp key (buffers by
       // column parity: a warp staging column jj+2 has passed column jj+1's barrier, so nobody still
@@ -207,19 +215,32 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
         el[j] = alive[j] && !zero_piv;
         l[j] = el[j] ? mul(a[j][u], rcp) : zero_of<T>();
       }
+      // column u+1 first, then its pivot search, then the rest
+      if (u + 1 < KB) {
+        T v1;
+        if constexpr (sizeof(T) == 8) {
+          const double2 pr = wpk[(u + 1) / 2];
+          v1 = from_d2<T>(make_double2(((u + 1) & 1) ? pr.y : pr.x, 0.0));
+        } else {
+          v1 = from_d2<T>(wpk[u + 1]);
+        }
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) fms_acc(a[j][u + 1], l[j], v1);
+      }
+      if (jj + 1 < kb) warp_best(u + 1, nwv, nwrow, nwlane, nbj);
       if constexpr (sizeof(T) == 8) {
 #pragma unroll
-        for (int c = (u + 1) / 2; c < KB / 2; ++c) {
+        for (int c = (u + 2) / 2; c < KB / 2; ++c) {
           const double2 v = wpk[c];
 #pragma unroll
           for (int j = 0; j < RPT; ++j) {
-            if (2 * c > u) fms_acc(a[j][2 * c], l[j], from_d2<T>(make_double2(v.x, 0.0)));
+            if (2 * c > u + 1) fms_acc(a[j][2 * c], l[j], from_d2<T>(make_double2(v.x, 0.0)));
             fms_acc(a[j][2 * c + 1], l[j], from_d2<T>(make_double2(v.y, 0.0)));
           }
         }
       } else {
 #pragma unroll
-        for (int c = u + 1; c < KB; ++c) {
+        for (int c = u + 2; c < KB; ++c) {
           const T v = from_d2<T>(wpk[c]);
 #pragma unroll
           for (int j = 0; j < RPT; ++j) fms_acc(a[j][c], l[j], v);
