@@ -192,6 +192,13 @@ struct LmDeviceState {
   int pad_[1];
 };
 
+// Gate of the core-system kernels (Phi, LU, inverse): gate_running 0 = always, 1 = while the fit
+// runs, 2 = while it runs and only after an accepted decision (the main core system when the
+// rejection branch was factored speculatively, engine.cu prepare_core)
+__device__ __forceinline__ bool lu_gated(const LmDeviceState* st, int gate_running) {
+  return st && gate_running && (st->stopped || st->err_code || (gate_running == 2 && !st->accepted));
+}
+
 struct IterRecordDev {
   double relerr, mu;
   int iter, accepted;

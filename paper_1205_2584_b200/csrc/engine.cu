@@ -144,6 +144,17 @@ struct Engine final : EngineBase {
   uint8_t *ozYA = nullptr, *ozYB = nullptr, *ozBA = nullptr, *ozBB = nullptr;
   int *ozFrowA = nullptr, *ozFrowB = nullptr, *ozFr = nullptr;  // ozFr: [0, 32) pass A, [32, 64) pass B
   double *ozM1 = nullptr, *ozZ = nullptr, *ozBp = nullptr;          // epilogue partial sums
+  // Speculative rejection branch (CPF_SPEC, plan_spec): at the start of an iteration the core
+  // system a rejection would need next -- Phi(Grams_t, mu_t * growth_t) -- is factored and inverted
+  // on its own streams (sS, sS2) into its own buffers, concurrently with the candidate and pass A.
+  // After a rejection the next iteration copies it in (k_copy gated kOnRejectPrev) and the fork's
+  // own core system is skipped (gate 2: accepted only); after an acceptance it is discarded.
+  bool use_spec = false, spec_capture = false;
+  T *PhiS = nullptr, *PhiInvS = nullptr, *TriTmpS = nullptr, *GtiS = nullptr, *GiS = nullptr, *invLS = nullptr;
+  int *ibufS = nullptr, *gringS = nullptr, *spec_sing = nullptr;
+  LuWork luS{};
+  cudaStream_t sS = nullptr, sS2 = nullptr;
+  cudaEvent_t evS0 = nullptr, evS1 = nullptr;
   int dm_nt = 0;
   DmmaGeom da{}, db{};
   size_t da_smem = 0, db_smem = 0;
@@ -183,6 +194,7 @@ struct Engine final : EngineBase {
   cudaEvent_t gmark[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   bool capturing = false;
   void mark(int id) {
+    if (spec_capture) return;
     if (gmarks && capturing) {
       if (!gmark[id]) CPF_CUDA_CHECK(cudaEventCreate(&gmark[id]));
       CPF_CUDA_CHECK(cudaEventRecordWithFlags(gmark[id], s, cudaEventRecordExternal));
@@ -272,13 +284,18 @@ struct Engine final : EngineBase {
     if (evJ) cudaEventDestroy(evJ);
     if (s2) cudaStreamDestroy(s2);
     if (evF) cudaEventDestroy(evF);
+    if (evS0) cudaEventDestroy(evS0);
+    if (evS1) cudaEventDestroy(evS1);
+    if (sS) cudaStreamDestroy(sS);
+    if (sS2) cudaStreamDestroy(sS2);
     if (evG) cudaEventDestroy(evG);
     if (s3) cudaStreamDestroy(s3);
     for (auto& e : evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     void* ptrs[] = {Yown, A, Ac, M, Mc, D, G, Cand, V1, V2, V3, V4, Cg, Ccg, Gx, Gp, Gf, Gti, Gi, W1, Sm,
                     wvec, fvec, xvec, Phi, A1c, KMc, WNc, A1r, KMr, WNr, zpart, m1part, bpart, pa_out, pb_out, pb_all,
                     norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL, WNd, KMd, gring, PhiInv, TriTmp, yvec, tmv_part,
-                    ozYA, ozYB, ozBA, ozBB, ozFrowA, ozFrowB, ozFr, ozM1, ozZ, ozBp};
+                    ozYA, ozYB, ozBA, ozBB, ozFrowA, ozFrowB, ozFr, ozM1, ozZ, ozBp,
+                    PhiS, PhiInvS, TriTmpS, GtiS, GiS, invLS, ibufS, gringS, spec_sing};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (hst) cudaFreeHost(hst);
@@ -410,6 +427,7 @@ struct Engine final : EngineBase {
     plan_v2(nsm);
     plan_dmma(nsm);
     plan_oz();
+    plan_spec();
     kLuReserveSms = use_oz ? 40 : 24;
     if (const char* e = getenv("CPF_LU_RESERVE")) kLuReserveSms = atoi(e);
     CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lu_smem));
@@ -567,6 +585,51 @@ struct Engine final : EngineBase {
       use_oz = true;
     }
   }
+  // speculative rejection branch (CPF_SPEC=1; off by default: at config 4 the slower pass A -- on
+  // 108 SMs and beside the branch's LU, 2.3 -> 2.7 ms -- costs more on the ~75 % accepted steps
+  // than the skipped LU saves on the rejected ones: 157.7 -> 151.7 it/s, parity tests green)
+  void plan_spec() {
+    use_spec = false;
+    if (const char* e = getenv("CPF_SPEC")) use_spec = e[0] == '1' && use_inv && lu3_rpt;
+    if (!use_spec) return;
+    const size_t R2 = (size_t)R * R;
+    PhiS = dalloc<T>((size_t)nB * nB);
+    PhiInvS = dalloc<T>((size_t)nB * nB);
+    TriTmpS = dalloc<T>((size_t)nB * nB);
+    GtiS = dalloc<T>(N * R2);
+    GiS = dalloc<T>(N * R2);
+    invLS = dalloc<T>(2 * kLuMaxKB * kLuMaxKB);
+    gringS = dalloc<int>(2 * (4 * kLuMaxKB + 4));
+    const int nblk32 = (nB + 31) / 32;
+    ibufS = dalloc<int>((size_t)2 * nB + 4 * kLuMaxKB + 8 + 2 * nblk32);
+    luS.perm = ibufS;
+    luS.ipiv = ibufS + nB;
+    luS.gather = ibufS + 2 * nB;
+    luS.gcount = luS.gather + 4 * kLuMaxKB;
+    luS.info = luS.gcount + 1;
+    luS.ticket = luS.info + 1;
+    luS.ready = luS.ticket + 4;
+    spec_sing = dalloc<int>(2);
+    int plo = 0, phi = 0;
+    CPF_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&plo, &phi));
+    CPF_CUDA_CHECK(cudaStreamCreateWithPriority(&sS, cudaStreamNonBlocking, phi));
+    CPF_CUDA_CHECK(cudaStreamCreateWithPriority(&sS2, cudaStreamNonBlocking, phi));
+    CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evS0, cudaEventDisableTiming));
+    CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evS1, cudaEventDisableTiming));
+  }
+  void swap_spec() {
+    std::swap(Phi, PhiS);
+    std::swap(PhiInv, PhiInvS);
+    std::swap(TriTmp, TriTmpS);
+    std::swap(Gti, GtiS);
+    std::swap(Gi, GiS);
+    std::swap(invL, invLS);
+    std::swap(gring, gringS);
+    std::swap(lu, luS);
+    std::swap(s, sS);
+    std::swap(s2, sS2);
+  }
+
   // one-time digit-plane images of the bound tensor (both passes), stream-ordered after the upload
   void oz_split() {
     if (!use_oz || Jloc == 0) return;
@@ -810,7 +873,8 @@ struct Engine final : EngineBase {
         const LmDeviceState* cst = st;
         const DevFlags* cfl = fl;
         launch(k_oz_split_b, dim3(R), 256, 0, (const double*)WNc, Cloc, R, RP, ozBA, ozFr, cst, cfl, gate);
-        const int nch = std::max(1, nsm_ / oa.nb);
+        // beside a speculated core system, pass A leaves the LU its SMs like pass B does
+        const int nch = std::max(1, (use_spec ? nsm_ - kLuReserveSms : nsm_) / oa.nb);
         const OzOut oo{(const double*)A1c, (const double*)KMc, RP, nch, (Lmid + nch - 1) / nch, ozM1, ozZ};
         launch(k_oz_pass<0>, dim3((unsigned)(oa.nb * nch)), kOzThreads, kOzSmem, (const uint8_t*)ozYA,
                (const int*)ozFrowA, (const uint8_t*)ozBA, (const int*)ozFr, oa, oo, cst, cfl, gate);
@@ -1123,7 +1187,7 @@ struct Engine final : EngineBase {
         CPF_CUDA_CHECK(cudaEventRecord(evB, s2));
       }
       CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evB, 0));
-      launch(k_lu_info_to_err, 1, 1, 0, (const int*)lu.info, st);
+      if (!spec_capture) launch(k_lu_info_to_err, 1, 1, 0, (const int*)lu.info, st);
       ph_end();
       return;
     }
@@ -1220,10 +1284,20 @@ struct Engine final : EngineBase {
   // fLM candidate at (A, cache, M, G) with the state's mu -> Cand  (solver.py:189-226)
   // Damped Gamma inverses for the state's mu, Phi and its LU: everything of the step that does
   // not depend on Y or the MTTKRPs (it only needs the Grams and mu)
-  void prepare_core(int gate) {
-    const int gr = gate == kRunning ? 1 : 0;
-    launch(k_damped_inverses<T>, 2 * N, 128, 2 * R * R * sizeof(T), (const T*)Gx, N, R, Gti, Gi, st,
-           (const DevFlags*)fl, gate, (const int*)kinv_ok, (const double*)nullptr);
+  // mode 0: the state's mu; 1: speculative rejection branch (buffers swapped in, mu * growth,
+  // errors deferred); 2: the fork's core system when a rejection branch was speculated (skipped
+  // after a rejection)
+  void prepare_core(int gate, int mode = 0) {
+    const int gr = mode == 2 ? 2 : (gate == kRunning ? 1 : 0);
+    if (mode == 1) {
+      launch(k_spec_begin, 1, 1, 0, (const LmDeviceState*)st, dscal + 8, spec_sing);
+      launch(k_damped_inverses<T>, 2 * N, 128, 2 * R * R * sizeof(T), (const T*)Gx, N, R, Gti, Gi, st,
+             (const DevFlags*)fl, gate, (const int*)nullptr, (const double*)(dscal + 8), spec_sing);
+    } else {
+      launch(k_damped_inverses<T>, 2 * N, 128, 2 * R * R * sizeof(T), (const T*)Gx, N, R, Gti, Gi, st,
+             (const DevFlags*)fl, mode == 2 ? (int)kOnAccept : gate, (const int*)kinv_ok, (const double*)nullptr,
+             (int*)nullptr);
+    }
     launch(k_phi_assemble<T>, nblocks((int64_t)nB * nB, 256), 256, 0, Phi, N, R, (const T*)Cg, (const T*)Gi,
            (const T*)Gp, (const T*)Gf, (const LmDeviceState*)st, gr);
     mark(5);
@@ -1501,6 +1575,32 @@ struct Engine final : EngineBase {
     const int g = kRunning;
     pdl_now = true;
     mark(0);
+    if (use_spec) {
+      // the previous step was rejected: its core system is the speculated one
+      const int gp = kOnRejectPrev;
+      launch(k_copy<T>, nblocks((int64_t)nB * nB, 256), 256, 0, (const T*)PhiInvS, PhiInv, (int64_t)nB * nB,
+             (const LmDeviceState*)st, (const DevFlags*)fl, gp);
+      launch(k_copy<int>, nblocks(nB, 256), 256, 0, (const int*)luS.perm, lu.perm, (int64_t)nB,
+             (const LmDeviceState*)st, (const DevFlags*)fl, gp);
+      launch(k_copy<T>, nblocks((int64_t)N * R * R, 256), 256, 0, (const T*)GtiS, Gti, (int64_t)N * R * R,
+             (const LmDeviceState*)st, (const DevFlags*)fl, gp);
+      launch(k_copy<T>, nblocks((int64_t)N * R * R, 256), 256, 0, (const T*)GiS, Gi, (int64_t)N * R * R,
+             (const LmDeviceState*)st, (const DevFlags*)fl, gp);
+      launch(k_spec_errors, 1, 1, 0, st, (const DevFlags*)fl, (const int*)spec_sing, (const int*)luS.info);
+      // this step's rejection branch, beside the candidate and pass A
+      CPF_CUDA_CHECK(cudaEventRecord(evS0, s));
+      CPF_CUDA_CHECK(cudaStreamWaitEvent(sS, evS0, 0));
+      pdl_now = false;
+      spec_capture = true;
+      swap_spec();
+      ls = s;
+      prepare_core(g, 1);
+      CPF_CUDA_CHECK(cudaEventRecord(evS1, s));
+      swap_spec();
+      ls = s;
+      spec_capture = false;
+      pdl_now = true;
+    }
     candidate(2, g, /*core_ready=*/true);  // Phi(mu_t, cache_t) was factored at the end of t-1
     mark(1);
     // delta' = cand - model (solver.py:348)
@@ -1534,7 +1634,7 @@ struct Engine final : EngineBase {
     if (serial) {  // diagnostic (CPF_SERIAL=1): no overlap, phases time standalone
       pass_b(A, M, ga);
       gradient(ga);
-      prepare_core(g);
+      prepare_core(g, use_spec ? 2 : 0);
     } else {
       CPF_CUDA_CHECK(cudaEventRecord(evF, s));
       CPF_CUDA_CHECK(cudaStreamWaitEvent(s3, evF, 0));
@@ -1543,10 +1643,11 @@ struct Engine final : EngineBase {
       gradient(ga);
       ls = s;
       CPF_CUDA_CHECK(cudaEventRecord(evG, s3));
-      prepare_core(g);
+      prepare_core(g, use_spec ? 2 : 0);
       CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evG, 0));
     }
     launch(k_clear_pending, 1, 1, 0, fl);
+    if (use_spec) CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evS1, 0));
     mark(4);
   }
 

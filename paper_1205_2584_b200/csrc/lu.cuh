@@ -51,7 +51,7 @@ template <class T>
 __global__ void __launch_bounds__(256) k_panel_lu(T* __restrict__ A, int n, int lda, int k0, int kb, int rpc, LuWork w,
                                                   const LmDeviceState* st, int gate_running) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -206,7 +206,7 @@ template <class T>
 __global__ void k_row_gather(T* __restrict__ A, int n, int lda, int k0, int kb, LuWork w, const LmDeviceState* st,
                              int gate_running) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int G = *w.gcount;
   if (G == 0) return;
@@ -241,7 +241,7 @@ __global__ void k_row_gather2(T* __restrict__ A, int lda, const int* __restrict_
                               int* __restrict__ perm, int ca0, int ca1, int cb0, int cb1, int do_perm,
                               const LmDeviceState* st, int gate_running) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int G = *gcount;
   if (G == 0) return;
@@ -273,7 +273,7 @@ template <class T, int KB>
 __global__ void k_trsm_llnu(T* __restrict__ A, int n, int lda, int k0, int kb, const LmDeviceState* st,
                             int gate_running) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   __shared__ T L[KB * KB];
   for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
     int i = e % kb, j = e / kb;
@@ -304,7 +304,7 @@ template <class T>
 __global__ void __launch_bounds__(256) k_gemm_sub(T* __restrict__ Mx, int lda, int r0, int c0, int k0, int m, int nn,
                                                   int k, const LmDeviceState* st, int gate_running) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   constexpr int TM = 64, TN = 64, BK = 16;
   __shared__ T As[BK][TM + 1];
   __shared__ T Bs[BK][TN + 1];
@@ -366,7 +366,7 @@ template <class T>
 __global__ void k_perm_gather(const T* __restrict__ b, const int* __restrict__ perm, int n, T* __restrict__ x,
                               const LmDeviceState* st, int gate_running) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q < n) x[q] = b[perm[q]];
 }
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(128) k_trsv(const T* __restrict__ A, int n, in
                                               int* __restrict__ ticket, int* __restrict__ ready, int epoch,
                                               const LmDeviceState* st, int gate_running) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   __shared__ int s_b;
   __shared__ T part[4][32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;

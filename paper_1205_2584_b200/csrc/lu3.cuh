@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
                                                        PanelPrev<T> pv) {
   pdl_wait();
   static_assert(KB == kLuMaxKB, "panel width");
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(256) k_u12(T* __restrict__ A, int cend, int ld
                                              const T* __restrict__ invL, const LmDeviceState* st, int gate_running,
                                              int cbeg) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   lu_trace(1, k0 / KB, 0);
   __shared__ T Li[KB * KB];
   __shared__ T Bt[KB * 64];
@@ -519,7 +519,7 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 __global__ void __launch_bounds__(128) k_gemm_dmma(double* __restrict__ M, int lda, int r0, int c0, int k0, int m,
                                                    int nn, int k, const LmDeviceState* st, int gate_running) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   lu_trace(2, k0 / 32, 0);
   constexpr int TM = 64, TN = 64, KM = 32, PADA = 68, PADB = 68;
   __shared__ double As[KM * PADA];  // As[q][i] (k-major), stride PADA

@@ -24,7 +24,7 @@ struct Modes {
 // Kernel gating.  kAlways: unconditional (preamble); kRunning: skip once the fit stopped;
 // kOnAccept: only while an accepted candidate is being committed (flags->pending_accept);
 // kOnDirect / kOnCurDirect: the guard-band direct residual of the candidate / current model.
-enum Gate : int { kAlways = 0, kRunning = 1, kOnAccept = 2, kOnDirect = 3, kOnCurDirect = 4 };
+enum Gate : int { kAlways = 0, kRunning = 1, kOnAccept = 2, kOnDirect = 3, kOnCurDirect = 4, kOnRejectPrev = 5 };
 
 struct DevFlags {
   int pending_accept;
@@ -38,6 +38,7 @@ __device__ __forceinline__ bool gate_open(const LmDeviceState* st, const DevFlag
   if (gate == kRunning) return st->stopped == 0;
   if (gate == kOnAccept) return fl->pending_accept != 0;
   if (gate == kOnDirect) return fl->need_direct != 0;
+  if (gate == kOnRejectPrev) return st->stopped == 0 && st->err_code == 0 && st->iter > 0 && !st->accepted;
   return fl->need_cur_direct != 0;
 }
 
@@ -139,7 +140,7 @@ __global__ void k_kernel_flag(const T* __restrict__ pair, int N, int R, LmDevice
 template <class T>
 __global__ void k_damped_inverses(const T* __restrict__ excl, int N, int R, T* __restrict__ Gti, T* __restrict__ Gi,
                                   LmDeviceState* st, const DevFlags* fl, int gate, const int* kinv_ok,
-                                  const double* mu_override) {
+                                  const double* mu_override, int* sing_out = nullptr) {
   pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -202,7 +203,8 @@ __global__ void k_damped_inverses(const T* __restrict__ excl, int N, int R, T* _
   T* out = (transposed ? Gti : Gi) + (int64_t)n * R2;
   for (int e = threadIdx.x; e < R2; e += blockDim.x) out[e] = a[e + R2];
   if (threadIdx.x == 0) {
-    if (sing_s && st->err_code == 0) { st->err_code = kErrSingular; }
+    if (sing_s && sing_out) *sing_out = 1;  // speculative branch: reported if it is taken
+    else if (sing_s && st->err_code == 0) { st->err_code = kErrSingular; }
     if (blockIdx.x == 0 && kinv_ok && st->variant == 2 && !*kinv_ok && st->err_code == 0)
       st->err_code = kErrKernelSingular;
   }
@@ -558,6 +560,22 @@ __global__ void k_copy2d(const T* __restrict__ src, int64_t lds, T* __restrict__
 
 __global__ void k_clear_pending(DevFlags* fl) {
   pdl_wait(); fl->pending_accept = 0; }
+
+// Speculative rejection branch (engine.cu): mu of the branch = mu * growth, exactly k_decide's
+// rejection update; its error flags are cleared first.
+__global__ void k_spec_begin(const LmDeviceState* st, double* mu_rej, int* sing) {
+  pdl_wait();
+  *mu_rej = st->mu * st->growth;
+  *sing = 0;
+}
+// After a rejection, the speculative branch's errors become the fit's (as the core system of a
+// rejected step would have reported them at the end of that step)
+__global__ void k_spec_errors(LmDeviceState* st, const DevFlags* fl, const int* sing, const int* info) {
+  pdl_wait();
+  if (!gate_open(st, fl, kOnRejectPrev)) return;
+  if (*sing) st->err_code = kErrSingular;
+  else if (*info != 0) st->err_code = st->use_kinv ? kErrSingular : kErrPhi1Singular;
+}
 
 // Guard band: the identity ||Y||^2 - 2Re<Y,X> + ||X||^2 has an absolute error of a
 // few eps * ||Y||^2.  When the accept decision is within that band of a tie, or the residual is

@@ -22,7 +22,7 @@ template <class T>
 __global__ void __launch_bounds__(64) k_tri_inv_diag(const T* __restrict__ LU, int n, T* __restrict__ Inv,
                                                      const LmDeviceState* st, int gate_running) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   __shared__ T blk[32][33];
   const int b0 = blockIdx.x * 32;
   const int bs = min(32, n - b0);
@@ -84,7 +84,7 @@ template <class T, int STEP>
 __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* __restrict__ Inv, T* __restrict__ Tmp,
                                                    int n, int s, const LmDeviceState* st, int gate_running) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   const int pair = blockIdx.z >> 1, tri = blockIdx.z & 1;
   const int b1 = 2 * pair * s, b2 = b1 + s;
   if (b2 >= n) return;
@@ -232,7 +232,7 @@ template <class T, bool LOWER>
 __global__ void __launch_bounds__(256) k_tri_mv(const T* __restrict__ Inv, int n, const T* __restrict__ x,
                                                 T* __restrict__ part, const LmDeviceState* st, int gate_running) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   __shared__ T red[4][kTmvRows];
   const int r0 = blockIdx.x * kTmvRows, c0 = blockIdx.y * kTmvCols;
   const int tid = threadIdx.x, rl = tid % kTmvRows, g = tid / kTmvRows;
@@ -265,7 +265,7 @@ template <class T, bool LOWER>
 __global__ void k_tri_mv_sum(const T* __restrict__ part, int nslices, int n, const T* __restrict__ x, T* __restrict__ y,
                              const LmDeviceState* st, int gate_running) {
   pdl_wait();
-  if (st && gate_running && (st->stopped || st->err_code)) return;
+  if (lu_gated(st, gate_running)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   T v = LOWER ? x[i] : zero_of<T>();
