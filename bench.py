@@ -295,10 +295,6 @@ def main():
         local_dims = tuple(cfg.dims[:-1]) + (hi - lo,)
         y_host = np.reshape(arr.T, local_dims, order="F")
         conf = FitConfig(rank=cfg.rank, variant="auto", tau=tau, tol=0.0, max_iters=K, seed=args.seed, init="random")
-        # one untimed warm-up call (first-touch mapping of the ~50 GB of engine buffers on a fresh
-        # box measured up to 0.4 s once per process); the timed call below does all of its work
-        fit(y_host, FitConfig(rank=cfg.rank, variant="auto", tau=tau, tol=0.0, max_iters=1, seed=args.seed,
-                              init="random"), device=local, distributed=ctx, slab_of=cfg.dims[-1])
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
