@@ -348,12 +348,23 @@ __global__ void __launch_bounds__(kOzThreads, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(base + (size_t)s * kOzStageBytes);
           const uint64_t bdesc = oz_desc_b(sa + kOzABytes);
+          // Plane i accumulates into columns 32 i .. 32 (i + nb_i) - 1.  Plane 0 (accumulate off at
+          // kb = 0) initialises columns 0..255; the d = 10 block (columns 256..287) is first
+          // written by plane 1, so at kb = 0 plane 1's last 32 columns are a separate MMA with
+          // accumulate off (else it would add stale TMEM contents of the previous tile).
           if (!(g.dbg & 2))
 #pragma unroll
-            for (int i = 0; i < kOzPlanes; ++i)
-              oz_mma(dcol + 32u * i, oz_desc_a(sa + i * kOzAPlane), bdesc,
-                     oz_idesc(kOzN * (kOzDmax - 1 - i < kOzPlanes ? kOzDmax - 1 - i : kOzPlanes)),
-                     (kb > 0 || i > 0) ? 1 : 0);
+            for (int i = 0; i < kOzPlanes; ++i) {
+              const int nbp = kOzDmax - 1 - i < kOzPlanes ? kOzDmax - 1 - i : kOzPlanes;  // B planes used
+              if (i == 1 && kb == 0 && 32 * (i + nbp) > 256) {
+                oz_mma(dcol + 32u, oz_desc_a(sa + kOzAPlane), bdesc, oz_idesc(kOzN * (nbp - 1)), 1);
+                oz_mma(dcol + 256u, oz_desc_a(sa + kOzAPlane), oz_desc_b(sa + kOzABytes + (nbp - 1) * kOzBPlane),
+                       oz_idesc(kOzN), 0);
+              } else {
+                oz_mma(dcol + 32u * i, oz_desc_a(sa + i * kOzAPlane), bdesc, oz_idesc(kOzN * nbp),
+                       (kb > 0 || i > 0) ? 1 : 0);
+              }
+            }
           oz_commit(&empty[s]);
           if (++s == kOzStages) { s = 0; ph ^= 1u; }
         }
