@@ -91,6 +91,10 @@ typedef struct {
 
 int cpf_abi_version(void);
 int cpf_device_count(int* n);
+/* Grow the device's stream-ordered memory pool (which engines allocate from and return to) to at
+ * least `bytes`, so a following engine's allocations are reuses instead of fresh mappings
+ * (process setup, like context creation; no reference counterpart). */
+int cpf_pool_reserve(int device, int64_t bytes);
 /* 128-byte NCCL unique id for a multi-GPU engine group (rank 0 creates, all ranks receive). */
 int cpf_nccl_unique_id(void* out128);
 

@@ -85,6 +85,7 @@ EXPORTED_SYMBOLS = (
     "cpf_engine_unfolding_gram",
     "cpf_engine_pass_impl",
     "cpf_engine_load_cptn",
+    "cpf_pool_reserve",
 )
 
 
@@ -133,6 +134,7 @@ def _declare(lib) -> None:
         "cpf_engine_unfolding_gram": (I, [P, I, P]),
         "cpf_engine_pass_impl": (I, [P]),
         "cpf_engine_load_cptn": (I, [P, ctypes.c_char_p, I64]),
+        "cpf_pool_reserve": (I, [I, I64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -156,6 +158,13 @@ def load():
         _declare(lib)
         _lib = lib
         return lib
+
+
+def pool_reserve(device: int, nbytes: int) -> None:
+    """Grow the device memory pool engines allocate from (see cpf_pool_reserve)."""
+    rc = load().cpf_pool_reserve(int(device), int(nbytes))
+    if rc != CPF_OK:
+        raise NativeError(f"cpf_pool_reserve failed ({rc})")
 
 
 def device_count() -> int:

@@ -270,8 +270,10 @@ struct Engine final : EngineBase {
       }
       NCCL_CHECK(ncclCommInitRank(&comm, world, id, wrank));
     }
+    configure_pool(dev);
     alloc();
     plan();
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));  // stream-ordered allocations visible to every stream
   }
 
   ~Engine() override {
@@ -297,16 +299,26 @@ struct Engine final : EngineBase {
                     ozYA, ozYB, ozBA, ozBB, ozFrowA, ozFrowB, ozFr, ozM1, ozZ, ozBp,
                     PhiS, PhiInvS, TriTmpS, GtiS, GiS, invLS, ibufS, gringS, spec_sing};
     for (void* p : ptrs)
-      if (p) cudaFree(p);
+      if (p) cudaFreeAsync(p, s);  // back to the device pool (kept for the next engine)
     if (hst) cudaFreeHost(hst);
     if (comm) ncclCommDestroy(comm);
     if (s) cudaStreamDestroy(s);
   }
 
+  // Device buffers come from the device's default stream-ordered pool with an unlimited release
+  // threshold: an engine's ~50 GB (config 4: tensor + digit-plane images) stays reserved after it
+  // closes and the next engine reuses it -- cudaFree/cudaMalloc of that much memory costs up to
+  // ~0.5 s per fit (measured inside fit()'s wall time).
+  static void configure_pool(int device) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
   template <class U>
   U* dalloc(size_t n) {
     void* p = nullptr;
-    CPF_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(U)));
+    CPF_CUDA_CHECK(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(U), s));
     CPF_CUDA_CHECK(cudaMemsetAsync(p, 0, std::max<size_t>(n, 1) * sizeof(U), s));
     return static_cast<U*>(p);
   }
@@ -680,9 +692,9 @@ struct Engine final : EngineBase {
       db_chunks = (int)((Lmid + db.m_per_cta - 1) / db.m_per_cta);
       WNd = dalloc<double>((size_t)Cloc * ws + 8);
       KMd = dalloc<double>((size_t)Lmid * ws + 8);
-      if (zpart) cudaFree(zpart);
-      if (m1part) cudaFree(m1part);
-      if (bpart) cudaFree(bpart);
+      if (zpart) cudaFreeAsync(zpart, s);
+      if (m1part) cudaFreeAsync(m1part, s);
+      if (bpart) cudaFreeAsync(bpart, s);
       zpart = dalloc<T>((size_t)da.tiles * Lmid * RP);
       m1part = dalloc<T>((size_t)std::max(da_groups, 1) * I1 * RP + (size_t)Cloc * db_chunks * db.tiles * RP);
       bpart = dalloc<T>((size_t)std::max<int64_t>(Cloc, 1) * db_chunks * db.tiles * RP);
@@ -759,9 +771,9 @@ struct Engine final : EngineBase {
       gb.m_per_cta = mper;
       gb_chunks = (int)((Lmid + mper - 1) / mper);
     }
-    if (zpart) cudaFree(zpart);
-    if (m1part) cudaFree(m1part);
-    if (bpart) cudaFree(bpart);
+    if (zpart) cudaFreeAsync(zpart, s);
+    if (m1part) cudaFreeAsync(m1part, s);
+    if (bpart) cudaFreeAsync(bpart, s);
     zpart = dalloc<T>((size_t)ga.tiles * Lmid * RP);
     m1part = dalloc<T>((size_t)ga_groups * I1 * RP);
     bpart = dalloc<T>((size_t)std::max<int64_t>(Cloc, 1) * gb_chunks * gb.tiles * RP);
@@ -1422,12 +1434,12 @@ struct Engine final : EngineBase {
     CPF_CUDA_CHECK(cudaSetDevice(dev));
     if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }  // Y pointer is baked into the graph
     if (where == 1) {
-      if (Yown) { CPF_CUDA_CHECK(cudaFree(Yown)); Yown = nullptr; }
+      if (Yown) { CPF_CUDA_CHECK(cudaFreeAsync(Yown, s)); Yown = nullptr; }
       Y = static_cast<const T*>(p);
     } else {
       if (!Yown) {
         void* q = nullptr;
-        CPF_CUDA_CHECK(cudaMalloc(&q, std::max<int64_t>(Jloc, 1) * sizeof(T)));
+        CPF_CUDA_CHECK(cudaMallocAsync(&q, std::max<int64_t>(Jloc, 1) * sizeof(T), s));
         Yown = static_cast<T*>(q);
       }
       if (Jloc > 0) CPF_CUDA_CHECK(cudaMemcpyAsync(Yown, p, Jloc * sizeof(T), cudaMemcpyHostToDevice, s));
@@ -1453,7 +1465,7 @@ struct Engine final : EngineBase {
     posix_fadvise(fd, 0, 0, POSIX_FADV_SEQUENTIAL);
     if (!Yown) {
       void* q = nullptr;
-      CPF_CUDA_CHECK(cudaMalloc(&q, std::max<int64_t>(Jloc, 1) * sizeof(T)));
+      CPF_CUDA_CHECK(cudaMallocAsync(&q, std::max<int64_t>(Jloc, 1) * sizeof(T), s));
       Yown = static_cast<T*>(q);
     }
     const int64_t bytes = Jloc * es;
@@ -1502,7 +1514,7 @@ struct Engine final : EngineBase {
     if (variant < 0 || variant > 2) throw ApiError(CPF_E_ARG, "unknown variant");
     reset_state(variant, 0.0, tol, max_iters);
     if (trace_cap < max_iters) {
-      if (dtrace) CPF_CUDA_CHECK(cudaFree(dtrace));
+      if (dtrace) CPF_CUDA_CHECK(cudaFreeAsync(dtrace, s));
       dtrace = dalloc<IterRecordDev>(std::max(max_iters, 1));
       trace_cap = max_iters;
     }
@@ -1862,6 +1874,23 @@ int guarded(cpf_engine* e, F&& f) {
 extern "C" {
 
 int cpf_abi_version(void) { return CPF_ABI_VERSION; }
+
+int cpf_pool_reserve(int device, int64_t bytes) {
+  if (cudaSetDevice(device) != cudaSuccess) return CPF_E_CUDA;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return CPF_E_CUDA;
+  uint64_t thr = ~0ull;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return CPF_E_CUDA;
+  cudaError_t e = cudaMallocAsync(&p, (size_t)std::max<int64_t>(bytes, 1), st);
+  if (e == cudaSuccess) e = cudaFreeAsync(p, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess) { cudaGetLastError(); return CPF_E_CUDA; }
+  return CPF_OK;
+}
 
 int cpf_device_count(int* n) {
   int c = 0;

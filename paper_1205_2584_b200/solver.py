@@ -24,6 +24,7 @@ LM_VARIANTS = ("flm-a", "flm-b", "auto")
 MU_OVERFLOW = 1e30                                                       # solver.py:47
 RHO_DENOM_GUARD = 1e-30                                                  # solver.py:48
 POLL_EVERY = 1
+_TIMING = bool(__import__("os").environ.get("CPF_FIT_TIMING"))
 
 
 @dataclass
@@ -217,12 +218,27 @@ def _check_lm(config: FitConfig):
 def _run_fit(eng, gdims, scalar_kind: str, config: FitConfig, rng) -> FitResult:
     """The LM loop on an engine whose tensor is bound (solver.py:319-384); closes the engine."""
     try:
+        tt = [time.monotonic()]
         init = _init_model(_Dims(gdims, scalar_kind), config, rng, eng)
         eng.set_factors(init.as_vector())
+        tt.append(time.monotonic())
         st = eng.fit_begin(config.variant, config.tau, config.tol, config.max_iters)
+        tt.append(time.monotonic())
+        first = True
         while st.stopped == _native.STOP_RUNNING:
             st = eng.fit_step(max(1, min(POLL_EVERY, config.max_iters)))
+            if first:
+                tt.append(time.monotonic())
+                first = False
+        tt.append(time.monotonic())
         recs = eng.trace(config.max_iters)
+        if _TIMING:
+            import sys as _sys
+
+            _sys.stderr.write("[fit timing] init %.1f | fit_begin (upload wait + preamble) %.1f | first step "
+                              "(graph capture) %.1f | remaining steps %.1f ms\n"
+                              % tuple(1e3 * (tt[i + 1] - tt[i]) for i in range(len(tt) - 1))
+                              if len(tt) == 5 else "")
         trace = [IterRecord(t, e, m, a) for (t, e, m, a) in recs]
         model = model_from_vector(eng.get_factors(), gdims, config.rank)
         result = FitResult(model, trace, _stop_reason(st), launches=eng.launch_count())
@@ -248,8 +264,14 @@ def fit(y, config: FitConfig, *, device=None, distributed=None, slab_of=None) ->
     gdims = y.dims if slab_of is None else tuple(y.dims[:-1]) + (int(slab_of),)
     rng = np.random.default_rng([config.seed, 0])
     eng = _make_engine(y, config.rank, device, distributed, slab_of)
+    t1 = time.monotonic()
     result = _run_fit(eng, gdims, y.scalar_kind, config, rng)
     result.time_ms = (time.monotonic() - t0) * 1e3
+    if _TIMING:
+        import sys as _sys
+
+        _sys.stderr.write(f"[fit timing] engine + tensor upload {1e3 * (t1 - t0):.1f} ms, "
+                          f"init + LM loop + download {1e3 * (time.monotonic() - t1):.1f} ms\n")
     return result
 
 
