@@ -23,6 +23,9 @@ VARIANTS = ("flm-a", "flm-b", "auto", "als", "als-ls", "dgn-oracle")   # solver.
 LM_VARIANTS = ("flm-a", "flm-b", "auto")
 MU_OVERFLOW = 1e30                                                       # solver.py:47
 RHO_DENOM_GUARD = 1e-30                                                  # solver.py:48
+# iterations per fit_step call: the engine polls its device-side stop flag every 4 graph replays
+# internally, so a fixed-length fit (tol = 0) runs in one call; with a tolerance, one call per
+# iteration keeps the trace exact without gated replays after the stop
 POLL_EVERY = 1
 _TIMING = bool(__import__("os").environ.get("CPF_FIT_TIMING"))
 
@@ -226,7 +229,7 @@ def _run_fit(eng, gdims, scalar_kind: str, config: FitConfig, rng) -> FitResult:
         tt.append(time.monotonic())
         first = True
         while st.stopped == _native.STOP_RUNNING:
-            st = eng.fit_step(max(1, min(POLL_EVERY, config.max_iters)))
+            st = eng.fit_step(config.max_iters if config.tol == 0.0 else max(1, min(POLL_EVERY, config.max_iters)))
             if first:
                 tt.append(time.monotonic())
                 first = False
