@@ -145,13 +145,24 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
       int* wkr_p = wkey_r + par * NW;
       if (lane == wlane) {
         T* dst = wrow_p + wid * KB;
+        if constexpr (sizeof(T) == 8) {  // 16-byte stores
 #pragma unroll
-        for (int q = 0; q < KB; ++q) {
-          T sel = a[0][q];
+          for (int q = 0; q < KB; q += 2) {
+            T s0 = a[0][q], s1 = a[0][q + 1];
 #pragma unroll
-          for (int j = 1; j < RPT; ++j)
-            if (bj == j) sel = a[j][q];
-          dst[q] = sel;
+            for (int j = 1; j < RPT; ++j)
+              if (bj == j) { s0 = a[j][q]; s1 = a[j][q + 1]; }
+            *reinterpret_cast<double2*>(dst + q) = make_double2(as_d2(s0).x, as_d2(s1).x);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < KB; ++q) {
+            T sel = a[0][q];
+#pragma unroll
+            for (int j = 1; j < RPT; ++j)
+              if (bj == j) sel = a[j][q];
+            dst[q] = sel;
+          }
         }
         wkv_p[wid] = wv;
         wkr_p[wid] = wrow;
