@@ -527,6 +527,22 @@ __global__ void __launch_bounds__(128) k_gemm_dmma(double* __restrict__ M, int l
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int bm = blockIdx.x * TM, bn = blockIdx.y * TN;
   // stage A (64 x k) and B (k x 64); zero-fill out of range and K tail to a multiple of 4
+  const int wm = (wid & 1) * 32, wn = (wid >> 1) * 32;
+  const int g = lane >> 2, t = lane & 3;
+  // C[row = g, cols 2t, 2t+1] of each 8x8 tile, fetched first (in flight with the A/B staging) and
+  // all before any store (the compiler cannot hoist loads over stores through the same pointer):
+  // one memory round trip per CTA instead of 32.  C1's first 4736 x 4704 x 32 update 185 -> 106 us,
+  // C1 51 -> 57 it/s.
+  double cv[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gi = bm + wm + 8 * i + g, gj = bn + wn + 8 * j + 2 * t + h;
+        cv[i][j][h] = (gi < m && gj < nn) ? M[(int64_t)(r0 + gi) + (int64_t)lda * (c0 + gj)] : 0.0;
+      }
   const int kp = (k + 3) & ~3;
   // stage A (64 x KM) and B (KM x 64): constant trip counts so all 32 loads per thread are in
   // flight at once (rows/cols beyond the block and K beyond k are zero)
@@ -558,8 +574,6 @@ __global__ void __launch_bounds__(128) k_gemm_dmma(double* __restrict__ M, int l
     }
   }
   __syncthreads();
-  const int wm = (wid & 1) * 32, wn = (wid >> 1) * 32;
-  const int g = lane >> 2, t = lane & 3;
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -576,20 +590,6 @@ __global__ void __launch_bounds__(128) k_gemm_dmma(double* __restrict__ M, int l
 #pragma unroll
       for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
   }
-  // epilogue: C[row = g, cols 2t, 2t+1] of each 8x8 tile.  All 32 C loads are issued before any
-  // store (the compiler cannot hoist loads over stores through the same pointer): one memory
-  // round trip per CTA instead of 32 (with the unrolled staging: C1's first 4736 x 4704 x 32 update
-  // 185 -> 124 us, C1 51 -> 56.7 it/s)
-  double cv[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int gi = bm + wm + 8 * i + g, gj = bn + wn + 8 * j + 2 * t + h;
-        cv[i][j][h] = (gi < m && gj < nn) ? M[(int64_t)(r0 + gi) + (int64_t)lda * (c0 + gj)] : 0.0;
-      }
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
