@@ -53,3 +53,9 @@ def test_substitution_solves(api, monkeypatch):
 def test_int8_passes_four_way(api, monkeypatch):
     monkeypatch.setenv("CPF_OZ", "1")
     _check(api, _problem((40, 9, 8, 7), 6, False, 7), 6)
+
+
+@pytest.mark.parametrize("dims,R", [((50, 40), 4), ((6, 5, 4, 5, 7), 3)])
+def test_int8_passes_order_2_and_5(api, monkeypatch, dims, R):
+    monkeypatch.setenv("CPF_OZ", "1")
+    _check(api, _problem(dims, R, False, 8), R)
