@@ -597,11 +597,12 @@ struct Engine final : EngineBase {
       use_oz = true;
     }
   }
-  // speculative rejection branch (CPF_SPEC=1; off by default: at config 4 the slower pass A -- on
-  // 108 SMs and beside the branch's LU, 2.3 -> 2.7 ms -- costs more on the ~75 % accepted steps
-  // than the skipped LU saves on the rejected ones: 157.7 -> 151.7 it/s, parity tests green)
+  // speculative rejection branch: on where the tensor passes are short next to the LU (FMA-pass
+  // tensors: C2 416 -> 446, C3 693 -> 732 it/s); off for the long int8 / DMMA passes (config 4:
+  // pass A on 108 SMs beside the branch's LU, 2.3 -> 2.7 ms, costs more on the ~75 % accepted
+  // steps than the skipped LU saves: 157.7 -> 151.7 it/s).  CPF_SPEC=0/1 overrides.
   void plan_spec() {
-    use_spec = false;
+    use_spec = use_inv && lu3_rpt && !use_oz && !use_dmma;
     if (const char* e = getenv("CPF_SPEC")) use_spec = e[0] == '1' && use_inv && lu3_rpt;
     if (!use_spec) return;
     const size_t R2 = (size_t)R * R;
