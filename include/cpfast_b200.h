@@ -152,6 +152,11 @@ int64_t cpf_engine_launch_count(const cpf_engine* e);
 #define CPF_PASS_DMMA 1
 #define CPF_PASS_OZAKI 2
 int cpf_engine_pass_impl(const cpf_engine* e);
+/* Accuracy guard of the int8 passes (diagnostic, no reference counterpart): number of tensor-pass
+ * launches since the last fit_begin whose K x R operand was outside the int8 split's accuracy
+ * envelope and that therefore ran in fp64 (*out); and whether the bound tensor itself was outside
+ * it (*tensor_rejected = 1: the engine planned fp64 passes for the whole tensor). */
+int cpf_engine_pass_guard(cpf_engine* e, int64_t* fallbacks, int* tensor_rejected);
 
 #ifdef __cplusplus
 }

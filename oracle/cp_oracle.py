@@ -403,9 +403,11 @@ def nielsen(mu: float, growth: float, rho: float):
     return mu * growth, 2.0 * growth, False
 
 
-def gain_ratio(prev_sq: float, cand_sq: float, delta: np.ndarray, grad: np.ndarray, mu: float) -> float:
-    """rho = (prev - cand) / Re<delta, g + mu delta> with the 1e-30 guard (solver.py:259-263)."""
-    denom = np.real(np.vdot(delta, grad + mu * delta))
+def gain_ratio(prev_sq: float, cand_sq: float, delta: np.ndarray, grad: np.ndarray, mu: float,
+               sign: float = 1.0) -> float:
+    """rho = (prev - cand) / Re<delta, g + mu delta> with the 1e-30 guard (solver.py:259-263).
+    ``sign = -1`` is a test hook (negated denominator, see OracleConfig.negate_denom_at)."""
+    denom = sign * np.real(np.vdot(delta, grad + mu * delta))
     if abs(denom) < RHO_DENOM_GUARD:
         return -1.0
     return (prev_sq - cand_sq) / denom
@@ -426,6 +428,10 @@ class OracleConfig:
     max_iters: int = 1000
     seed: int = 0
     init: str = "random"
+    # test hook, not reference behaviour: negate the gain-ratio denominator at this iteration so a
+    # worse candidate gets rho > 0 -- the "rho > 0 but cand_err >= err" rejection of solver.py:361
+    # (mirrors the engine's CPF_TEST_NEGDENOM)
+    negate_denom_at: int = 0
 
 
 @dataclass
@@ -486,7 +492,7 @@ def fit_lm(y, cfg: OracleConfig, init_factors=None, on_iter=None) -> OracleResul
         cand_err = relative_error(y, cand)
         cand_sq = (cand_err * ynorm) ** 2
         grad = gradient_from_mttkrps(A, g, M)
-        rho = gain_ratio(err_sq, cand_sq, delta, grad, mu)
+        rho = gain_ratio(err_sq, cand_sq, delta, grad, mu, -1.0 if t == cfg.negate_denom_at else 1.0)
         mu, growth, ok = nielsen(mu, growth, rho)
         detail.append((err_sq, cand_sq, rho))
         if ok and cand_err < err:

@@ -84,6 +84,7 @@ EXPORTED_SYMBOLS = (
     "cpf_engine_launch_count",
     "cpf_engine_unfolding_gram",
     "cpf_engine_pass_impl",
+    "cpf_engine_pass_guard",
     "cpf_engine_load_cptn",
     "cpf_pool_reserve",
 )
@@ -133,6 +134,7 @@ def _declare(lib) -> None:
         "cpf_engine_launch_count": (I64, [P]),
         "cpf_engine_unfolding_gram": (I, [P, I, P]),
         "cpf_engine_pass_impl": (I, [P]),
+        "cpf_engine_pass_guard": (I, [P, ctypes.POINTER(I64), ctypes.POINTER(I)]),
         "cpf_engine_load_cptn": (I, [P, ctypes.c_char_p, I64]),
         "cpf_pool_reserve": (I, [I, I64]),
     }
@@ -332,3 +334,9 @@ class Engine:
 
     def pass_impl(self) -> int:
         return int(self._lib.cpf_engine_pass_impl(self._h))
+
+    def pass_guard(self) -> tuple[int, bool]:
+        """(int8-pass launches that fell back to fp64 since fit_begin, tensor rejected by the guard)."""
+        fb, rej = ctypes.c_int64(0), ctypes.c_int(0)
+        self._check(self._lib.cpf_engine_pass_guard(self._h, ctypes.byref(fb), ctypes.byref(rej)))
+        return int(fb.value), bool(rej.value)

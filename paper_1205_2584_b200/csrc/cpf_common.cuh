@@ -189,14 +189,20 @@ struct LmDeviceState {
   int cand_zero;             // normalised candidate had a zero-norm column (raise on accept)
   int err_direct;            // err/err_sq come from a direct residual (not the identity)
   int force_direct;          // evaluate every trial fit directly (cheap-pass / LU-bound regime)
-  int pad_[1];
+  int rej_grow;              // last decision took the rho <= 0 branch (mu *= growth): the only
+                             // case whose next core system is Phi(Grams_t, mu_t * growth_t), i.e.
+                             // the speculated one.  A rho > 0 rejection (cand_err >= err) shrinks
+                             // mu instead and needs a freshly factored core system.
+  int test_negdenom_iter;    // test hook (CPF_TEST_NEGDENOM=t): negate the gain-ratio denominator
+                             // at iteration t to force a rho > 0 / not-improved rejection
+  int pad_[2];
 };
 
 // Gate of the core-system kernels (Phi, LU, inverse): gate_running 0 = always, 1 = while the fit
-// runs, 2 = while it runs and only after an accepted decision (the main core system when the
-// rejection branch was factored speculatively, engine.cu prepare_core)
+// runs, 2 = while it runs unless the last decision was a rho <= 0 rejection (the main core system
+// when that rejection branch was factored speculatively, engine.cu prepare_core)
 __device__ __forceinline__ bool lu_gated(const LmDeviceState* st, int gate_running) {
-  return st && gate_running && (st->stopped || st->err_code || (gate_running == 2 && !st->accepted));
+  return st && gate_running && (st->stopped || st->err_code || (gate_running == 2 && st->rej_grow));
 }
 
 struct IterRecordDev {

@@ -80,6 +80,7 @@ struct EngineBase {
   virtual void phase_times(double* ms, int64_t* cnt, int n) = 0;
   virtual int64_t launches() const = 0;
   virtual int pass_impl() const = 0;
+  virtual void pass_guard(int64_t* fallbacks, int* rejected) = 0;
   virtual void unfolding_gram(int mode, void* out) = 0;
 };
 
@@ -581,6 +582,16 @@ struct Engine final : EngineBase {
       const size_t need = ((size_t)oa.ntiles * oa.nkb + (size_t)ob.ntiles * ob.nkb) * kOzABytes;
       size_t free_b = 0, total_b = 0;
       CPF_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+      // memory the stream-ordered pool holds but does not use is available to this engine too
+      // (cudaMemGetInfo counts it as used; the pool never releases it, see configure_pool)
+      {
+        cudaMemPool_t pool;
+        uint64_t reserved = 0, used = 0;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+          free_b += (size_t)(reserved - used);
+      }
       if (!force && need + ((size_t)2 << 30) + (size_t)Jloc * sizeof(T) > free_b) return;
       ozYA = dalloc<uint8_t>((size_t)oa.ntiles * oa.nkb * kOzABytes);
       ozYB = dalloc<uint8_t>((size_t)ob.ntiles * ob.nkb * kOzABytes);
@@ -643,14 +654,33 @@ struct Engine final : EngineBase {
     std::swap(s2, sS2);
   }
 
-  // one-time digit-plane images of the bound tensor (both passes), stream-ordered after the upload
+  // one-time digit-plane images of the bound tensor (both passes), stream-ordered after the upload.
+  // Accuracy guard (tensor_pass_oz.cuh): if any row of either pass's view of Y is outside the int8
+  // split's envelope, the engine drops the int8 passes for this tensor and stays on fp64.
+  bool oz_y_rejected = false;
   void oz_split() {
     if (!use_oz || Jloc == 0) return;
     if constexpr (sizeof(T) == 8) {
       const double* Yd = reinterpret_cast<const double*>(Y);
-      k_oz_rowexp<0><<<nsm_ * 8, 256, 0, s>>>(Yd, oa, ozFrowA);
+      int* ybad = reinterpret_cast<int*>(red);  // scratch
+      CPF_CUDA_CHECK(cudaMemsetAsync(ybad, 0, sizeof(int), s));
+      k_oz_rowexp<0><<<nsm_ * 8, 256, 0, s>>>(Yd, oa, ozFrowA, ybad);
+      k_oz_rowexp<1><<<nsm_ * 8, 256, 0, s>>>(Yd, ob, ozFrowB, ybad);
+      CPF_CUDA_CHECK(cudaGetLastError());
+      int nbad = 0;
+      CPF_CUDA_CHECK(cudaMemcpyAsync(&nbad, ybad, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+      if (nbad > 0) {
+        oz_y_rejected = true;
+        use_oz = false;
+        CPF_CUDA_CHECK(cudaFreeAsync(ozYA, s));
+        CPF_CUDA_CHECK(cudaFreeAsync(ozYB, s));
+        ozYA = ozYB = nullptr;
+        kLuReserveSms = 24;
+        if (const char* e = getenv("CPF_LU_RESERVE")) kLuReserveSms = atoi(e);
+        return;
+      }
       k_oz_split_y<0><<<nsm_ * 16, 256, 0, s>>>(Yd, oa, ozFrowA, ozYA);
-      k_oz_rowexp<1><<<nsm_ * 8, 256, 0, s>>>(Yd, ob, ozFrowB);
       k_oz_split_y<1><<<nsm_ * 16, 256, 0, s>>>(Yd, ob, ozFrowB, ozYB);
       CPF_CUDA_CHECK(cudaGetLastError());
     }
@@ -877,26 +907,57 @@ struct Engine final : EngineBase {
       launch(k_conj_rowmajor<T>, nblocks(Cloc * RP, 256), 256, 0, F + offs[N - 1], Cloc, slab_lo, IN, R, RP, WNc, (const LmDeviceState*)st, (const DevFlags*)fl, gate, 1);
   }
 
+  int* oz_bad_ptr(int pass) {
+    return reinterpret_cast<int*>(reinterpret_cast<char*>(fl) + offsetof(DevFlags, oz_bad)) + pass * kOzGuardCols;
+  }
+
   // Pass A at factors F -> out modes 1..N-1 of Mout (stacked), allreduced.
+  // Int8 (Ozaki) passes: the operand split also checks the accuracy envelope; the int8 kernels are
+  // gated on it and the fp64 pass below runs instead when the operand is outside it.
   void pass_a(const T* F, T* Mout, int gate) {
     prep_operands(F, true, gate);
     ph_begin(kPhPassA);
+    bool oz = false;
     if constexpr (sizeof(T) == 8) {
       if (Cloc > 0 && use_oz) {
+        oz = true;
         const LmDeviceState* cst = st;
         const DevFlags* cfl = fl;
-        launch(k_oz_split_b, dim3(R), 256, 0, (const double*)WNc, Cloc, R, RP, ozBA, ozFr, cst, cfl, gate);
+        const int go = gate | kGateIfOzOk, gf = gate | kGateIfOzBad;
+        launch(k_oz_split_b, dim3(R), 256, 0, (const double*)WNc, Cloc, R, RP, ozBA, ozFr, oz_bad_ptr(0), cst, cfl,
+               gate);
         // beside a speculated core system, pass A leaves the LU its SMs like pass B does
         const int nch = std::max(1, (use_spec ? nsm_ - kLuReserveSms : nsm_) / oa.nb);
         const OzOut oo{(const double*)A1c, (const double*)KMc, RP, nch, (Lmid + nch - 1) / nch, ozM1, ozZ};
         launch(k_oz_pass<0>, dim3((unsigned)(oa.nb * nch)), kOzThreads, kOzSmem, (const uint8_t*)ozYA,
-               (const int*)ozFrowA, (const uint8_t*)ozBA, (const int*)ozFr, oa, oo, cst, cfl, gate);
+               (const int*)ozFrowA, (const uint8_t*)ozBA, (const int*)ozFr, oa, oo, cst, cfl, go);
         ph_end();
-        launch(k_m1_reduce<T>, nblocks(I1 * R, 32), 256, 0, (const T*)ozM1, nch, I1, R, RP, pa_out, cst, cfl, gate);
+        launch(k_m1_reduce<T>, nblocks(I1 * R, 32), 256, 0, (const T*)ozM1, nch, I1, R, RP, pa_out, cst, cfl, go);
         launch(k_z_reduce<T>, nblocks(Lmid * R, 256), 256, 0, (const T*)ozZ, oa.nb, Lmid, R, RP, pa_out + I1 * R,
-               cst, cfl, gate);
-        goto pass_a_done;
+               cst, cfl, go);
+        launch(k_oz_note_fallback, 1, 1, 0, fl, cst, gf);
+        pass_a_fp64(F, gf);
       }
+    }
+    if (!oz) pass_a_fp64(F, gate);
+    if (comm) {
+      NCCL_CHECK(ncclAllReduce(pa_out, pa_out, (size_t)(I1 + Lmid) * R * (sizeof(T) / sizeof(double)), ncclDouble,
+                               ncclSum, comm, s));
+    }
+    // scatter: M_1 = pa_out[0 : I1 R]; N==3: M_2 = Z; N>=4: M_2..M_{N-1} from Z (at F)
+    launch(k_copy<T>, nblocks(I1 * R, 256), 256, 0, (const T*)pa_out, Mout + offs[0], I1 * R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    if (N == 3) {
+      launch(k_copy<T>, nblocks(Lmid * R, 256), 256, 0, (const T*)(pa_out + I1 * R), Mout + offs[1], Lmid * R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    } else if (N >= 4) {
+      for (int k = 0; k < N - 2; ++k)
+        launch(k_mid_mttkrp<T>, nblocks(mg.dims[k] * R, 128), 128, 0, (const T*)(pa_out + I1 * R), Lmid, F, mg, k, R,
+               Mout + offs[k + 1], (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    }
+  }
+
+  // fp64 pass A (DMMA / staged DFMA / plain) -> pa_out partial sums of this slab
+  void pass_a_fp64(const T* F, int gate) {
+    if constexpr (sizeof(T) == 8) {
       if (Cloc > 0 && use_dmma) {
         const LmDeviceState* cst = st;
         const DevFlags* cfl = fl;
@@ -913,7 +974,7 @@ struct Engine final : EngineBase {
                gate);
         launch(k_z_reduce<T>, nblocks(Lmid * R, 256), 256, 0, (const T*)zpart, da.tiles, Lmid, R, RP, pa_out + I1 * R,
                cst, cfl, gate);
-        goto pass_a_done;
+        return;
       }
     }
     if (Cloc > 0 && use_v2) {
@@ -946,46 +1007,70 @@ struct Engine final : EngineBase {
       ph_end();
       CPF_CUDA_CHECK(cudaMemsetAsync(pa_out, 0, sizeof(T) * (I1 + Lmid) * R, s));
     }
-  pass_a_done:
-    if (comm) {
-      NCCL_CHECK(ncclAllReduce(pa_out, pa_out, (size_t)(I1 + Lmid) * R * (sizeof(T) / sizeof(double)), ncclDouble,
-                               ncclSum, comm, s));
-    }
-    // scatter: M_1 = pa_out[0 : I1 R]; N==3: M_2 = Z; N>=4: M_2..M_{N-1} from Z (at F)
-    launch(k_copy<T>, nblocks(I1 * R, 256), 256, 0, (const T*)pa_out, Mout + offs[0], I1 * R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
-    if (N == 3) {
-      launch(k_copy<T>, nblocks(Lmid * R, 256), 256, 0, (const T*)(pa_out + I1 * R), Mout + offs[1], Lmid * R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
-    } else if (N >= 4) {
-      for (int k = 0; k < N - 2; ++k)
-        launch(k_mid_mttkrp<T>, nblocks(mg.dims[k] * R, 128), 128, 0, (const T*)(pa_out + I1 * R), Lmid, F, mg, k, R,
-               Mout + offs[k + 1], (const LmDeviceState*)st, (const DevFlags*)fl, gate);
-    }
   }
 
-  // Pass B at factors F -> mode N of Mout (allgathered).
+  // Pass B at factors F -> mode N of Mout (allgathered).  Int8 passes: guarded like pass A.
   void pass_b(const T* F, T* Mout, int gate) {
     prep_operands(F, false, gate);
     ph_begin(kPhPassB);
-    int nparts = pb_chunks * pb_tiles;
-    bool done_b = false, oz_b = false;
+    struct Red { const T* src; int nparts; int gate; };
+    Red reds[2];
+    int nred = 0;
+    bool oz = false;
     if constexpr (sizeof(T) == 8) {
       if (Cloc > 0 && use_oz) {
+        oz = true;
+        const int go = gate | kGateIfOzOk | kGateOzPass, gf = gate | kGateIfOzBad | kGateOzPass;
         // overlapped with the next LU (ls != s): leave kLuReserveSms SMs to the panel clusters
         const int grid = ls != s ? std::max(1, nsm_ - kLuReserveSms) : nsm_;
-        launch(k_oz_split_b, dim3(R), 256, 0, (const double*)KMc, Lmid, R, RP, ozBB, ozFr + kOzN,
+        launch(k_oz_split_b, dim3(R), 256, 0, (const double*)KMc, Lmid, R, RP, ozBB, ozFr + kOzN, oz_bad_ptr(1),
                (const LmDeviceState*)st, (const DevFlags*)fl, gate);
         const int nch = std::max(1, grid / ob.nb);
         const OzOut oo{(const double*)A1c, nullptr, RP, nch, (Cloc + nch - 1) / nch, nullptr, ozBp};
         launch(k_oz_pass<1>, dim3((unsigned)(ob.nb * nch)), kOzThreads, kOzSmem, (const uint8_t*)ozYB,
                (const int*)ozFrowB, (const uint8_t*)ozBB, (const int*)(ozFr + kOzN), ob, oo, (const LmDeviceState*)st,
-               (const DevFlags*)fl, gate);
-        nparts = ob.nb;
-        done_b = oz_b = true;
+               (const DevFlags*)fl, go);
+        ph_end();
+        launch(k_oz_note_fallback, 1, 1, 0, fl, (const LmDeviceState*)st, gf);
+        reds[nred++] = Red{(const T*)ozBp, ob.nb, go};
+        reds[nred++] = Red{(const T*)bpart, pass_b_fp64(F, gf), gf};
       }
-      if (Cloc > 0 && use_dmma && !oz_b) {
+    }
+    if (!oz) {
+      reds[nred++] = Red{(const T*)bpart, pass_b_fp64(F, gate), gate};
+      ph_end();
+    }
+    // M_N rows of this slab from the partial sums
+    auto mn_rows = [&](T* dst, int64_t ldm) {
+      for (int i = 0; i < nred; ++i)
+        launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, reds[i].src, Cloc, reds[i].nparts, R, RP, ldm, dst,
+               (const LmDeviceState*)st, (const DevFlags*)fl, reds[i].gate);
+    };
+    if (!comm) {
+      mn_rows(Mout + offs[N - 1], IN);
+    } else {
+      CPF_CUDA_CHECK(cudaMemsetAsync(pb_out, 0, sizeof(T) * Cpad * R, ls));
+      if (Cloc > 0) mn_rows(pb_out, Cpad);
+      const size_t cnt = (size_t)Cpad * R * (sizeof(T) / sizeof(double));
+      NCCL_CHECK(ncclAllGather(pb_out, pb_all, cnt, ncclDouble, comm, ls));
+      // pb_all[rank][c + Cpad r] -> Mout_N[(rank*Cpad + c) + IN r]
+      for (int q = 0; q < world; ++q) {
+        const int64_t lo = std::min<int64_t>(IN, (int64_t)q * Cpad);
+        const int64_t cnt_rows = std::min<int64_t>(IN, lo + Cpad) - lo;
+        if (cnt_rows <= 0) continue;
+        launch(k_copy2d<T>, nblocks(cnt_rows * R, 256), 256, 0, (const T*)(pb_all + (size_t)q * Cpad * R), Cpad,
+               Mout + offs[N - 1] + lo, IN, cnt_rows, (int64_t)R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+      }
+    }
+  }
+
+  // fp64 pass B (DMMA / staged DFMA / plain) -> bpart; returns the number of partials per row
+  int pass_b_fp64(const T* F, int gate) {
+    if (Cloc <= 0) return 1;
+    if constexpr (sizeof(T) == 8) {
+      if (use_dmma) {
         const LmDeviceState* cst = st;
         const DevFlags* cfl = fl;
-        nparts = db_chunks * db.tiles;
         if (N == 3)
           launch(k_conj_rowmajor<T>, nblocks(Lmid * db.WS, 256), 256, 0, (const T*)(F + offs[1]), Lmid, (int64_t)0, Lmid,
                  R, db.WS, (T*)KMd, cst, cfl, gate, 1);
@@ -1005,12 +1090,10 @@ struct Engine final : EngineBase {
                    (double*)bpart, cst, cfl, gate);
           }
         });
-        done_b = true;
+        return db_chunks * db.tiles;
       }
     }
-    if (done_b) {
-    } else if (Cloc > 0 && use_v2) {
-      nparts = gb_chunks * gb.tiles;
+    if (use_v2) {
       dispatch_rp([&](auto rpc) {
         constexpr int RPc = decltype(rpc)::value;
         if (rpt == 2) {
@@ -1022,36 +1105,15 @@ struct Engine final : EngineBase {
                  (const T*)A1c, (const T*)KMc, bpart, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
         }
       });
-    } else if (Cloc > 0) {
-      dispatch_rp([&](auto rpc) {
-        constexpr int RPc = decltype(rpc)::value;
-        const size_t smem = sizeof(T) * RPc * ((pb_threads + 31) / 32);
-        launch(k_pass_b<T, RPc>, dim3((unsigned)Cloc, pb_chunks, pb_tiles), dim3(pb_threads), smem, Y, I1, Lmid,
-               Cloc, (const T*)A1c, (const T*)KMc, pb_TI, pb_TM, pb_mper, bpart, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
-      });
+      return gb_chunks * gb.tiles;
     }
-    ph_end();
-    // M_N rows of this slab from the partial sums (Ozaki passes: one partial per i1 block)
-    auto mn_rows = [&](T* dst, int64_t ldm) {
-      launch(k_pass_b_reduce<T>, nblocks(Cloc * R, 256), 256, 0, oz_b ? (const T*)ozBp : (const T*)bpart, Cloc,
-             nparts, R, RP, ldm, dst, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
-    };
-    if (!comm) {
-      mn_rows(Mout + offs[N - 1], IN);
-    } else {
-      CPF_CUDA_CHECK(cudaMemsetAsync(pb_out, 0, sizeof(T) * Cpad * R, ls));
-      if (Cloc > 0) mn_rows(pb_out, Cpad);
-      const size_t cnt = (size_t)Cpad * R * (sizeof(T) / sizeof(double));
-      NCCL_CHECK(ncclAllGather(pb_out, pb_all, cnt, ncclDouble, comm, ls));
-      // pb_all[rank][c + Cpad r] -> Mout_N[(rank*Cpad + c) + IN r]
-      for (int q = 0; q < world; ++q) {
-        const int64_t lo = std::min<int64_t>(IN, (int64_t)q * Cpad);
-        const int64_t cnt_rows = std::min<int64_t>(IN, lo + Cpad) - lo;
-        if (cnt_rows <= 0) continue;
-        launch(k_copy2d<T>, nblocks(cnt_rows * R, 256), 256, 0, (const T*)(pb_all + (size_t)q * Cpad * R), Cpad,
-               Mout + offs[N - 1] + lo, IN, cnt_rows, (int64_t)R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
-      }
-    }
+    dispatch_rp([&](auto rpc) {
+      constexpr int RPc = decltype(rpc)::value;
+      const size_t smem = sizeof(T) * RPc * ((pb_threads + 31) / 32);
+      launch(k_pass_b<T, RPc>, dim3((unsigned)Cloc, pb_chunks, pb_tiles), dim3(pb_threads), smem, Y, I1, Lmid,
+             Cloc, (const T*)A1c, (const T*)KMc, pb_TI, pb_TM, pb_mper, bpart, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
+    });
+    return pb_chunks * pb_tiles;
   }
 
   // ||Y - X(F)||^2 computed directly (guard band, preamble, relative_error API) -> *out (device)
@@ -1302,13 +1364,12 @@ struct Engine final : EngineBase {
   // after a rejection)
   void prepare_core(int gate, int mode = 0) {
     const int gr = mode == 2 ? 2 : (gate == kRunning ? 1 : 0);
-    if (mode == 1) {
-      launch(k_spec_begin, 1, 1, 0, (const LmDeviceState*)st, dscal + 8, spec_sing);
+    if (mode == 1) {  // mu * growth snapshot: k_spec_begin on the main stream (iteration())
       launch(k_damped_inverses<T>, 2 * N, 128, 2 * R * R * sizeof(T), (const T*)Gx, N, R, Gti, Gi, st,
              (const DevFlags*)fl, gate, (const int*)nullptr, (const double*)(dscal + 8), spec_sing);
     } else {
       launch(k_damped_inverses<T>, 2 * N, 128, 2 * R * R * sizeof(T), (const T*)Gx, N, R, Gti, Gi, st,
-             (const DevFlags*)fl, mode == 2 ? (int)kOnAccept : gate, (const int*)kinv_ok, (const double*)nullptr,
+             (const DevFlags*)fl, mode == 2 ? (int)kOnCoreNeeded : gate, (const int*)kinv_ok, (const double*)nullptr,
              (int*)nullptr);
     }
     launch(k_phi_assemble<T>, nblocks((int64_t)nB * nB, 256), 256, 0, Phi, N, R, (const T*)Cg, (const T*)Gi,
@@ -1571,6 +1632,9 @@ struct Engine final : EngineBase {
       hst->force_direct = pass_flops < 0.05 * lu_flops ? 1 : 0;
       if (const char* e = getenv("CPF_FORCE_DIRECT")) hst->force_direct = (e[0] == '1');
     }
+    hst->rej_grow = 0;
+    hst->test_negdenom_iter = 0;
+    if (const char* e = getenv("CPF_TEST_NEGDENOM")) hst->test_negdenom_iter = atoi(e);  // test hook
     // keep use_kinv computed by the cache kernels
     LmDeviceState tmp;
     CPF_CUDA_CHECK(cudaMemcpyAsync(&tmp, st, sizeof(tmp), cudaMemcpyDeviceToHost, s));
@@ -1600,7 +1664,9 @@ struct Engine final : EngineBase {
       launch(k_copy<T>, nblocks((int64_t)N * R * R, 256), 256, 0, (const T*)GiS, Gi, (int64_t)N * R * R,
              (const LmDeviceState*)st, (const DevFlags*)fl, gp);
       launch(k_spec_errors, 1, 1, 0, st, (const DevFlags*)fl, (const int*)spec_sing, (const int*)luS.info);
-      // this step's rejection branch, beside the candidate and pass A
+      // this step's rejection branch, beside the candidate and pass A; its mu is snapshotted on s
+      // (ordered before this iteration's k_decide), the branch itself only reads dscal[8]
+      launch(k_spec_begin, 1, 1, 0, (const LmDeviceState*)st, dscal + 8, spec_sing);
       CPF_CUDA_CHECK(cudaEventRecord(evS0, s));
       CPF_CUDA_CHECK(cudaStreamWaitEvent(sS, evS0, 0));
       pdl_now = false;
@@ -1807,6 +1873,14 @@ struct Engine final : EngineBase {
   }
   int64_t launches() const override { return nlaunch; }
   int pass_impl() const override { return use_oz ? CPF_PASS_OZAKI : use_dmma ? CPF_PASS_DMMA : CPF_PASS_FMA; }
+  void pass_guard(int64_t* fallbacks, int* rejected) override {
+    int n = 0;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(&n, reinterpret_cast<const char*>(fl) + offsetof(DevFlags, oz_fallbacks), sizeof(int),
+                                   cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (fallbacks) *fallbacks = n;
+    if (rejected) *rejected = oz_y_rejected ? 1 : 0;
+  }
 
   // G_n = Y_(n) Y_(n)^H on the device (sum of the slab partials across ranks for n < N)
   void unfolding_gram(int mode, void* out) override {
@@ -2009,6 +2083,11 @@ int cpf_engine_phase_times(cpf_engine* e, double* ms_out, int64_t* counts_out, i
 
 int64_t cpf_engine_launch_count(const cpf_engine* e) { return (e && e->impl) ? e->impl->launches() : 0; }
 int cpf_engine_pass_impl(const cpf_engine* e) { return (e && e->impl) ? e->impl->pass_impl() : -1; }
+
+int cpf_engine_pass_guard(cpf_engine* e, int64_t* fallbacks, int* tensor_rejected) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->pass_guard(fallbacks, tensor_rejected); });
+}
 
 int cpf_engine_unfolding_gram(cpf_engine* e, int mode, void* out) {
   if (!e || !e->impl) return CPF_E_STATE;

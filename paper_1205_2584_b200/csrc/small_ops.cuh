@@ -24,21 +24,44 @@ struct Modes {
 // Kernel gating.  kAlways: unconditional (preamble); kRunning: skip once the fit stopped;
 // kOnAccept: only while an accepted candidate is being committed (flags->pending_accept);
 // kOnDirect / kOnCurDirect: the guard-band direct residual of the candidate / current model.
-enum Gate : int { kAlways = 0, kRunning = 1, kOnAccept = 2, kOnDirect = 3, kOnCurDirect = 4, kOnRejectPrev = 5 };
+// kOnRejectPrev: the previous decision was a rho <= 0 rejection (its core system was speculated);
+// kOnCoreNeeded: running and not kOnRejectPrev (the fork must factor the next core system).
+enum Gate : int { kAlways = 0, kRunning = 1, kOnAccept = 2, kOnDirect = 3, kOnCurDirect = 4, kOnRejectPrev = 5,
+                  kOnCoreNeeded = 6 };
 
+// Ozaki accuracy guard (tensor_pass_oz.cuh): per pass (0 = A, 1 = B) and operand column r,
+// oz_bad[pass][r] != 0 when that column of this launch's K x R operand is outside the int8 split's
+// accuracy envelope; the pass then runs in fp64 instead.  Composite gates: kGateIfOzOk / kGateIfOzBad
+// OR-ed into a base gate (bit kGateOzPass selects the pass) additionally require every / some column
+// flag clear / set.
+constexpr int kOzGuardCols = 32;
 struct DevFlags {
   int pending_accept;
   int need_direct;
   int need_cur_direct;
-  int pad;
+  int oz_fallbacks;                   // passes this fit that ran in fp64 because of the guard
+  int oz_bad[2][kOzGuardCols];
 };
+constexpr int kGateBaseMask = 0xff;
+constexpr int kGateIfOzOk = 0x100;
+constexpr int kGateIfOzBad = 0x200;
+constexpr int kGateOzPass = 0x400;  // set: pass B's flags
 
 __device__ __forceinline__ bool gate_open(const LmDeviceState* st, const DevFlags* fl, int gate) {
+  if (gate & (kGateIfOzOk | kGateIfOzBad)) {
+    const int* f = fl->oz_bad[(gate & kGateOzPass) ? 1 : 0];
+    int any = 0;
+#pragma unroll 4
+    for (int r = 0; r < kOzGuardCols; ++r) any |= f[r];
+    if ((gate & kGateIfOzOk) ? any != 0 : any == 0) return false;
+    gate &= kGateBaseMask;
+  }
   if (gate == kAlways) return true;
   if (gate == kRunning) return st->stopped == 0;
   if (gate == kOnAccept) return fl->pending_accept != 0;
   if (gate == kOnDirect) return fl->need_direct != 0;
-  if (gate == kOnRejectPrev) return st->stopped == 0 && st->err_code == 0 && st->iter > 0 && !st->accepted;
+  if (gate == kOnRejectPrev) return st->stopped == 0 && st->err_code == 0 && st->iter > 0 && st->rej_grow;
+  if (gate == kOnCoreNeeded) return st->stopped == 0 && !st->rej_grow;
   return fl->need_cur_direct != 0;
 }
 
@@ -562,7 +585,8 @@ __global__ void k_clear_pending(DevFlags* fl) {
   pdl_wait(); fl->pending_accept = 0; }
 
 // Speculative rejection branch (engine.cu): mu of the branch = mu * growth, exactly k_decide's
-// rejection update; its error flags are cleared first.
+// rho <= 0 update; its error flags are cleared first.  Launched on the main stream BEFORE the
+// branch forks off, so the snapshot is stream-ordered ahead of this iteration's k_decide.
 __global__ void k_spec_begin(const LmDeviceState* st, double* mu_rej, int* sing) {
   pdl_wait();
   *mu_rej = st->mu * st->growth;
@@ -611,7 +635,8 @@ __global__ void k_decide(LmDeviceState* st, DevFlags* fl, IterRecordDev* trace, 
     st->err_iter = t;
     return;
   }
-  const double yx = scal[0], xx = scal[2], denom = scal[3];
+  const double yx = scal[0], xx = scal[2];
+  const double denom = (t == st->test_negdenom_iter) ? -scal[3] : scal[3];
   const bool direct = fl->need_direct != 0;
   if (fl->need_cur_direct) {  // re-anchor the current error on a direct residual (kruskal.py:159-167)
     const double e0 = sqrt(scal[5]) / st->ynorm;
@@ -671,6 +696,7 @@ __global__ void k_decide(LmDeviceState* st, DevFlags* fl, IterRecordDev* trace, 
   }
   st->cand_zero = 0;
   st->accepted = acc;
+  st->rej_grow = ok ? 0 : 1;
   st->deltas[st->ndeltas % 10] = d;
   st->ndeltas += 1;
   trace[t - 1].relerr = st->err;

@@ -95,10 +95,29 @@ __device__ __forceinline__ int64_t oz_yidx(const OzGeom& g, int64_t i1, int64_t 
   return MODE == 0 ? i1 + g.I1 * (o + g.Lmid * k) : i1 + g.I1 * (k + g.Lmid * o);
 }
 
+// ---- accuracy envelope ------------------------------------------------------------------------
+// The split represents every element of a row (column) in fixed point against the row's max: an
+// element within 16x of the max is exact, a smaller one carries an absolute error <= 2^-57 * 2^e
+// (2^(e-1) <= max < 2^e).  The rigorous error of one K-term contraction is therefore
+//     E_oz <= 2^-56 (ymax ||b||_1 + bmax ||y||_1) + (dropped digit pairs, ~2^-58 K ymax bmax).
+// The guard keeps the int8 path only while every row of Y and every column of the operand has a
+// peak-to-rms ratio <= 16 (max^2 K <= 256 sum x^2): then E_oz <= 2^-51 K rms_y rms_b, i.e. a few
+// units of fp64 rounding on the K-term dot product's natural scale -- the scale of fp64's own
+// accumulation error for such data.  Spikier data (a few entries carrying the row) is outside that
+// envelope and the pass runs in fp64 (DMMA): Y is checked once when the tensor is bound (the plan
+// drops the int8 images), the operand on every launch (k_oz_split_b sets DevFlags::oz_bad, which
+// gates the int8 kernels off and the fp64 fallback on for that launch).
+constexpr double kOzPeakRms2 = 256.0;
+
+__device__ __forceinline__ bool oz_outside(double amax, double sumsq, int64_t K) {
+  return amax * amax * (double)K > kOzPeakRms2 * sumsq;
+}
+
 // ---- one-time split of Y into a pass's tile images ------------------------------------------
-// row exponents: thread per tile row (t, row); F = 0 for padding rows
+// row exponents: thread per tile row (t, row); F = 0 for padding rows.  *ybad counts the rows
+// outside the accuracy envelope (cleared by the host before the launch).
 template <int MODE>
-__global__ void k_oz_rowexp(const double* __restrict__ Y, OzGeom g, int* __restrict__ Frow) {
+__global__ void k_oz_rowexp(const double* __restrict__ Y, OzGeom g, int* __restrict__ Frow, int* __restrict__ ybad) {
   pdl_wait();
   const int64_t K = MODE == 0 ? g.C : g.Lmid;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < g.ntiles * kOzM;
@@ -107,10 +126,15 @@ __global__ void k_oz_rowexp(const double* __restrict__ Y, OzGeom g, int* __restr
     const int row = (int)(idx - t * kOzM);
     const int64_t o = t / g.nb;
     const int64_t i1 = (int64_t)kOzM * (t - o * g.nb) + row;
-    double m = 0.0;
+    double m = 0.0, ss = 0.0;
     if (i1 < g.I1)
-      for (int64_t k = 0; k < K; ++k) m = fmax(m, fabs(Y[oz_yidx<MODE>(g, i1, o, k)]));
+      for (int64_t k = 0; k < K; ++k) {
+        const double v = Y[oz_yidx<MODE>(g, i1, o, k)];
+        m = fmax(m, fabs(v));
+        ss = fma(v, v, ss);
+      }
     Frow[idx] = oz_scale_exp(m);
+    if (oz_outside(m, ss, K)) atomicAdd(ybad, 1);
   }
 }
 
@@ -156,25 +180,47 @@ __global__ void k_oz_split_y(const double* __restrict__ Y, OzGeom g, const int* 
 // (r) x 2 K chunks of 16 bytes: byte (r, k) at kb*8192 + j*1024 + (r/8)*256 + (k%32/16)*128 + (r%8)*16 + k%16
 // (the canonical K-major no-swizzle UMMA layout: LBO = 128 B between K chunks, SBO = 256 B between
 // 8-row groups).  Columns r >= R and rows k >= K stay zero (buffer cleared at allocation).
+// The block of column r also writes bad[r] (the accuracy guard: 1 = outside the envelope).
 __global__ void k_oz_split_b(const double* __restrict__ src, int64_t K, int R, int ld, uint8_t* __restrict__ Bq,
-                             int* __restrict__ Fr, const LmDeviceState* st, const DevFlags* fl, int gate) {
+                             int* __restrict__ Fr, int* __restrict__ bad, const LmDeviceState* st, const DevFlags* fl,
+                             int gate) {
   pdl_wait();
   if (!gate_open(st, fl, gate)) return;
   const int r = blockIdx.x;
-  __shared__ double red[32];
-  double m = 0.0;
-  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) m = fmax(m, fabs(src[k * ld + r]));
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __shared__ double red[32], red2[32];
+  double m = 0.0, ss = 0.0;
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+    const double v = src[k * ld + r];
+    m = fmax(m, fabs(v));
+    ss = fma(v, v, ss);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = m;
+    red2[threadIdx.x >> 5] = ss;
+  }
   __syncthreads();
   if (threadIdx.x < 32) {
     double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (threadIdx.x == 0) red[0] = v;
+    double w = threadIdx.x < (blockDim.x >> 5) ? red2[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+      w += __shfl_xor_sync(0xffffffffu, w, o);
+    }
+    if (threadIdx.x == 0) {
+      red[0] = v;
+      red2[0] = w;
+    }
   }
   __syncthreads();
   const int F = oz_scale_exp(red[0]);
-  if (threadIdx.x == 0) Fr[r] = F;
+  if (threadIdx.x == 0) {
+    Fr[r] = F;
+    if (bad && r < kOzGuardCols) bad[r] = oz_outside(red[0], red2[0], K) ? 1 : 0;
+  }
   const int64_t rofs = (int64_t)(r >> 3) * 256 + (r & 7) * 16;
   for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
     int8_t d[kOzPlanes];
@@ -184,6 +230,13 @@ __global__ void k_oz_split_b(const double* __restrict__ src, int64_t K, int R, i
 #pragma unroll
     for (int p = 0; p < kOzPlanes; ++p) dst[p * kOzBPlane] = (uint8_t)d[p];
   }
+}
+
+// counts the launches whose operand fell outside the envelope (gated kGateIfOzBad)
+__global__ void k_oz_note_fallback(DevFlags* fl, const LmDeviceState* st, int gate) {
+  pdl_wait();
+  if (!gate_open(st, fl, gate)) return;
+  atomicAdd(&fl->oz_fallbacks, 1);
 }
 
 // ---- tcgen05 / TMA primitives ---------------------------------------------------------------

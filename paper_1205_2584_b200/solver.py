@@ -64,6 +64,11 @@ class FitResult:
     stop_reason: str
     time_ms: float = 0.0
     launches: int = field(default=0, repr=False)
+    # engine diagnostics (no reference counterpart): tensor-pass implementation (_native.PASS_*),
+    # int8-pass launches that ran in fp64 under the accuracy guard, tensor rejected by the guard
+    pass_impl: int = field(default=-1, repr=False)
+    pass_fallbacks: int = field(default=0, repr=False)
+    tensor_guarded: bool = field(default=False, repr=False)
 
     @property
     def iters(self) -> int:
@@ -244,7 +249,9 @@ def _run_fit(eng, gdims, scalar_kind: str, config: FitConfig, rng) -> FitResult:
                               if len(tt) == 5 else "")
         trace = [IterRecord(t, e, m, a) for (t, e, m, a) in recs]
         model = model_from_vector(eng.get_factors(), gdims, config.rank)
-        result = FitResult(model, trace, _stop_reason(st), launches=eng.launch_count())
+        fallbacks, rejected = eng.pass_guard()
+        result = FitResult(model, trace, _stop_reason(st), launches=eng.launch_count(), pass_impl=eng.pass_impl(),
+                           pass_fallbacks=fallbacks, tensor_guarded=rejected)
         if st.stopped == _native.STOP_ERROR and st.err_code == _native.ERR_ZERO_COLUMN:
             raise ZeroDivisionError("a component of the accepted candidate has a zero-norm vector")
     finally:

@@ -129,9 +129,23 @@ def reconstruct_exact(factors) -> np.ndarray:
     return x
 
 
+_FSUM_CHUNK = 1 << 22
+
+
 def frob_exact(x: np.ndarray) -> float:
-    a = np.abs(x) ** 2 if np.iscomplexobj(x) else x * x
-    return math.sqrt(math.fsum(a.ravel(order="K").tolist()))
+    """Frobenius norm with exact (fsum) accumulation; above 2^22 elements the exact sums of
+    2^22-element chunks (Fortran order) are fsum-ed -- still machine independent, without a
+    J-element Python list."""
+    flat = x.ravel(order="F") if x.flags.f_contiguous else x.ravel(order="K")
+    if flat.size <= _FSUM_CHUNK:
+        a = np.abs(flat) ** 2 if np.iscomplexobj(flat) else flat * flat
+        return math.sqrt(math.fsum(a.tolist()))
+    parts = []
+    for lo in range(0, flat.size, _FSUM_CHUNK):
+        blk = flat[lo:lo + _FSUM_CHUNK]
+        a = np.abs(blk) ** 2 if np.iscomplexobj(blk) else blk * blk
+        parts.append(math.fsum(a.tolist()))
+    return math.sqrt(math.fsum(parts))
 
 
 def make_tensor(cfg: SynthConfig, seed: int = 0) -> np.ndarray:

@@ -1,0 +1,53 @@
+"""GPU parity at the benchmarked construction, on the engine's default planning.
+
+BASELINE config 4 (1000x1000x2000 fp64, R=20, c=0.7, SNR 20 dB, tol 0, 20 iterations) on its 1/8 slab
+1000x1000x250 -- the largest size whose reference run fits this container's RAM (the full tensor
+needs ~63 GB in the reference).  The golden (tests/golden/make_c4_slab_golden.py) is cpfast.fit's own
+trace and factors on bytes the GPU box regenerates (digest checked).  J = 2.5e8 puts the fit on the
+int8 tensor-core (Ozaki) passes by default, exactly like the benchmark: the test asserts that plan,
+that the accuracy guard never fell back, an identical accept/reject sequence, every recorded fit
+within 1e-10 and the final factors within 1e-9 (relative Frobenius) -- the north-star tolerances."""
+
+import numpy as np
+import pytest
+
+from tests import _golden as G
+from tests.test_gpu_parity import FACTOR_RTOL, FIT_ATOL, _rel
+
+pytestmark = pytest.mark.gpu
+
+NAME = "fit_c4_slab_s0_auto"
+
+
+@pytest.fixture(scope="module")
+def api(engine_lib):
+    import paper_1205_2584_b200 as api
+
+    return api
+
+
+@pytest.mark.slow
+def test_c4_slab_matches_reference_on_default_int8_path(api):
+    from paper_1205_2584_b200 import _native, synth
+
+    d = G.load_fit(NAME)
+    assert d["oracle_bitwise"], "the oracle reproduced this golden bit-for-bit when it was captured"
+    y = synth.make_tensor(G.synth_config(d), d["seed"])
+    assert synth.tensor_digest(y) == d["digest"], "regenerated input differs from the golden input"
+    conf = api.FitConfig(rank=d["rank"], variant=d["variant"], tau=d["tau"], tol=d["tol"],
+                         max_iters=d["max_iters"], seed=d["seed"], init="random")
+    res = api.fit(y, conf)
+    assert res.pass_impl == _native.PASS_OZAKI, "config-4 class tensors run on the int8 passes by default"
+    assert not res.tensor_guarded and res.pass_fallbacks == 0
+    ref_seq = G.accept_seq(d["trace"])
+    got_seq = "".join("A" if r.accepted else "r" for r in res.trace)
+    assert got_seq == ref_seq and res.stop_reason == d["stop_reason"]
+    errs = np.array([r.relerr for r in res.trace])
+    mus = np.array([r.mu for r in res.trace])
+    fit_dev = float(np.max(np.abs(errs - d["trace"][:, 1])))
+    mu_dev = float(np.max(np.abs(mus - d["trace"][:, 2]) / d["trace"][:, 2]))
+    fac_dev = _rel(res.model.as_vector(), d["factors"])
+    print(f"{NAME}: max |relerr - ref| = {fit_dev:.3e} (bound {FIT_ATOL:g}), max rel mu dev = {mu_dev:.3e}, "
+          f"factors rel = {fac_dev:.3e} (bound {FACTOR_RTOL:g})")
+    assert fit_dev < FIT_ATOL
+    assert fac_dev < FACTOR_RTOL
