@@ -16,7 +16,8 @@ Contract:
     J_local * 8 per launch over its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs;
   * cpu_baseline / --impl reference = the reference algorithm (oracle/cp_oracle.py, a call-for-
     call NumPy restatement of cpfast pinned bit-exact against the reference) on the host cores,
-    on a bounded slab sample of the same workload, extrapolated linearly in J.
+    on a bounded sample of the same construction (1000x1000x32 at config 4), the same iteration
+    window as the GPU arm; its tensor-sized time is scaled by J_full / J_sample.
 """
 
 from __future__ import annotations
@@ -102,61 +103,86 @@ class ClockSampler:
 # ----------------------------------------------------------------------------------------------
 # CPU reference arm (oracle = call-for-call restatement of cpfast, bounded slab sample)
 # ----------------------------------------------------------------------------------------------
+SAMPLE_ELEMS = 3.2e7   # ~256 MB fp64: one reference iteration is O(1 s) on the host, the whole
+                       # --steps/--warmup run a few minutes; the full config-4 tensor would need
+                       # ~63 GB of host RAM in the reference and ~30-300 s per iteration
+
+
+def host_info() -> dict:
+    """What the CPU numbers ran on: cores, affinity, cgroup quota, RAM, BLAS threads."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        info["affinity_cpus"] = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    try:
+        q = Path("/sys/fs/cgroup/cpu.max").read_text().split()
+        info["cgroup_cpu_max"] = None if q[0] == "max" else round(int(q[0]) / int(q[1]), 2)
+    except Exception:
+        pass
+    try:
+        mem = {ln.split(":")[0]: int(ln.split()[1]) for ln in Path("/proc/meminfo").read_text().splitlines()
+               if ln.startswith(("MemTotal", "MemAvailable"))}
+        info["ram_total_gb"] = round(mem["MemTotal"] / 2**20, 1)
+        info["ram_available_gb"] = round(mem["MemAvailable"] / 2**20, 1)
+    except Exception:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+
+        info["blas"] = [{k: d.get(k) for k in ("internal_api", "version", "num_threads")} for d in threadpool_info()]
+    except Exception:
+        pass
+    info["OPENBLAS_NUM_THREADS"] = os.environ.get("OPENBLAS_NUM_THREADS")
+    return info
+
+
 def cpu_sample_config(cfg):
-    """Bounded sample of the workload: same dims except the last mode, cut so that one reference
-    iteration takes O(1-5) s on the host (the reference needs ~4x the tensor in RAM)."""
+    """Bounded sample of the workload: the same construction (synth.make_tensor) with
+    the last mode cut so the sample has ~SAMPLE_ELEMS elements."""
     from paper_1205_2584_b200 import synth
 
     j = int(np.prod(cfg.dims))
-    target = 1.25e8  # elements (1 GB fp64)
-    if j <= target:
+    if j <= SAMPLE_ELEMS:
         return cfg, 1.0
-    last = max(1, int(cfg.dims[-1] * target / j))
+    last = max(1, int(math.ceil(cfg.dims[-1] * SAMPLE_ELEMS / j)))
     small = synth.scaled(cfg, tuple(cfg.dims[:-1]) + (last,), name=cfg.name + "_sample")
     return small, j / float(np.prod(small.dims))
 
 
-def fast_tensor(cfg, seed):
-    """Sample tensor for the CPU timing (BLAS path is fine here: timing, not parity)."""
-    from paper_1205_2584_b200 import synth
-
-    fac = synth.truth_factors(cfg, seed) if np.prod(cfg.dims) < 2e7 else None
-    rng = np.random.default_rng([seed, 100])
-    if fac is None:
-        fac = []
-        for d in cfg.dims:
-            q, _ = np.linalg.qr(rng.standard_normal((d, cfg.rank)))
-            fac.append(q)
-    kr = fac[0]
-    for f in fac[1:-1]:
-        kr = (f[:, None, :] * kr[None, :, :]).reshape(-1, cfg.rank)
-    x = (kr @ fac[-1].T).reshape(tuple(cfg.dims), order="F")
-    sigma = np.linalg.norm(x) / math.sqrt(x.size * 10.0 ** (cfg.snr_db / 10.0))
-    x += sigma * np.random.default_rng([seed, 1]).standard_normal(x.shape)
-    return np.asfortranarray(x)
-
-
-def run_cpu_reference(cfg, seed, iters, warmup=1):
-    """Time `iters` reference iterations (after `warmup`) on a sample; returns it/s at full size."""
+def run_cpu_reference(cfg, seed, steps, warmup):
+    """The reference fLM loop (oracle port) for warmup + steps iterations on the sample -- the same
+    iteration window as the GPU arm.  Per iteration the oracle reports the J-independent time (fLM
+    candidate incl. the NR^2 core inverse, gradient, decision) and the tensor-sized time (trial
+    relative error, and the N MTTKRPs of an accepted step); the full-size estimate scales only the
+    latter by J_full / J_sample."""
     from oracle import cp_oracle
     from paper_1205_2584_b200 import synth
 
     small, scale = cpu_sample_config(cfg)
-    y = fast_tensor(small, seed)
-    stamps = {}
+    y = synth.make_tensor(small, seed)
+    stamps, phases = {}, []
 
     def on_iter(t):
         stamps[t] = time.perf_counter()
 
     conf = cp_oracle.OracleConfig(rank=small.rank, tau=synth.tau_for_unit_mu(small, seed), tol=0.0,
-                                  max_iters=warmup + iters, seed=seed)
-    cp_oracle.fit_lm(y, conf, on_iter=on_iter)
-    dt = stamps[warmup + iters] - stamps[warmup]
-    per_sample = iters / dt
-    desc = (f"reference fLM (oracle/cp_oracle.py, bit-exact restatement of cpfast) on a "
-            f"{'x'.join(map(str, small.dims))} slab of the {'x'.join(map(str, cfg.dims))} tensor, R={cfg.rank}, "
-            f"{iters} timed iterations after {warmup} warm-up; it/s extrapolated x{scale:.2f} (linear in J)")
-    return per_sample / scale, desc, os.cpu_count()
+                                  max_iters=warmup + steps, seed=seed)
+    res = cp_oracle.fit_lm(y, conf, on_iter=on_iter, phases=phases)
+    timed = phases[warmup:warmup + steps]
+    sample_s = stamps[warmup + steps] - stamps[warmup]
+    core_s = sum(p[0] for p in timed)
+    tensor_s = sum(p[1] for p in timed)
+    full_s = core_s + scale * tensor_s
+    accepted = sum(1 for t in res.trace[warmup:warmup + steps] if t[3])
+    sample = (f"reference fLM (oracle/cp_oracle.py, bit-exact restatement of cpfast, pinned to cpfast goldens) on "
+              f"{'x'.join(map(str, small.dims))} (same construction as {'x'.join(map(str, cfg.dims))}), R={cfg.rank}, "
+              f"iterations {warmup + 1}..{warmup + steps} timed after {warmup} warm-up"
+              + (f"; full size = J-independent time + {scale:.2f} x tensor-sized time" if scale != 1.0 else ""))
+    return {"value": steps / full_s, "ms_per_step": 1e3 * sample_s / steps, "sample_it_s": steps / sample_s,
+            "scale_J": scale, "core_ms_per_step": 1e3 * core_s / steps, "tensor_ms_per_step": 1e3 * tensor_s / steps,
+            "accepted": accepted, "steps": steps, "warmup": warmup, "sample": sample,
+            "cores": os.cpu_count(), "host": host_info()}
 
 
 def line(d):
@@ -182,14 +208,23 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        iters = max(1, min(args.steps, 3))
-        v, desc, cores = run_cpu_reference(cfg, args.seed, iters, warmup=min(args.warmup, 1))
-        line({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-              "steps": iters, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 / v, "higher_is_better": True,
-              "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-              "config": config_desc,
-              "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc},
-              "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+        r = run_cpu_reference(cfg, args.seed, args.steps, args.warmup)
+        extrap = {"sample_value": r["sample_it_s"], "scale_J": r["scale_J"],
+                  "core_ms_per_step": r["core_ms_per_step"], "tensor_ms_per_step": r["tensor_ms_per_step"],
+                  "model": "full-size it/s = K / (sum of J-independent time + scale_J * sum of tensor-sized time)",
+                  "why": "the full config-4 tensor needs ~63 GB of host RAM in the reference (4x the tensor) and "
+                         "~30-300 s per iteration; the host record shows the RAM"}
+        line({"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+              "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+              "scaling": "strong", "vs_baseline": None, "dtype": "f64" if not cfg.complex_ else "c128",
+              "data": "synthetic", "config": config_desc,
+              "value_is": "extrapolated to the full config from the measured sample (ms_per_step is the sample's)"
+                          if r["scale_J"] != 1.0 else "measured",
+              "extrapolation": extrap if r["scale_J"] != 1.0 else None,
+              "accepted_in_timed": r["accepted"], "host": r["host"],
+              "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
+                               "sample": r["sample"]},
+              "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
         return
 
     import torch
@@ -211,16 +246,46 @@ def main():
     lo, hi = slab_bounds(cfg.dims[-1], world, rank)
     kind = _native.CPF_COMPLEX if cfg.complex_ else _native.CPF_REAL
     esize = 16 if cfg.complex_ else 8
+    rt = cfg.rank * sum(cfg.dims)
     y_dev = synth.device_tensor(cfg, args.seed, device=f"cuda:{local}", slab=(lo, hi))
     torch.cuda.synchronize()
     ctx = _Dist() if world > 1 else None
+    tau = synth.tau_for_unit_mu(cfg, args.seed)
+    K, W = args.steps, args.warmup
+
+    # ---- end to end through the public API, tensor in pinned HOST memory.  Run first, in a process
+    # whose engine memory pool is still empty: the cold call pays the pool's first-time mapping of the
+    # fit's ~50 GB; the warm call (after the device-resident timing) is a long-lived process's fit().
+    y_host = None
+    e2e_runs = {}
+
+    def run_e2e(tag):
+        conf = FitConfig(rank=cfg.rank, variant="auto", tau=tau, tol=0.0, max_iters=K, seed=args.seed, init="random")
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        res = fit(y_host, conf, device=local, distributed=ctx, slab_of=cfg.dims[-1])
+        wall = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([wall], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall = float(t.item())
+        e2e_runs[tag] = (res.iters / wall, res)
+
+    if not args.no_e2e:
+        host = torch.empty(y_dev.shape, dtype=y_dev.dtype, pin_memory=True)
+        host.copy_(y_dev)
+        torch.cuda.synchronize()
+        local_dims = tuple(cfg.dims[:-1]) + (hi - lo,)
+        y_host = np.reshape(host.numpy().T, local_dims, order="F")
+        run_e2e("cold")
+
+    # ---- device-resident throughput
     uid = ctx.unique_id() if ctx else None
     eng = _native.Engine(kind, cfg.dims, cfg.rank, local, rank, world, uid)
     eng.set_tensor_device(y_dev.data_ptr(), y_dev.numel())
     init = np.concatenate([f.reshape(-1, order="F") for f in synth.init_factors(cfg, args.seed)])
     eng.set_factors(init)
-    tau = synth.tau_for_unit_mu(cfg, args.seed)
-    K, W = args.steps, args.warmup
     NP = 3  # extra eagerly-launched, event-profiled iterations for the per-phase roofline numbers
     eng.fit_begin("auto", tau, 0.0, W + K + NP)
     eng.fit_step(W)  # warm-up (also captures the per-iteration CUDA graph)
@@ -241,6 +306,9 @@ def main():
     ms = ev0.elapsed_time(ev1)
     iters_done = st.iter - W
     launches = eng.launch_count() - launches0
+    trace = eng.trace(W + K)
+    accepted = sum(1 for t in trace[W:W + K] if t[3])
+    fallbacks, guarded = eng.pass_guard()
     # per-phase device times from CUDA events on the engine stream (eager launches)
     eng.profile(True)
     ms0, cnt0 = eng.phase_times()
@@ -253,12 +321,14 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = iters_done / (ms / 1e3)
+    ms_step = ms / max(iters_done, 1)
 
     # roofline of pass A (every-iteration tensor pass)
     pk, pk_kind = peaks()
     na = cnt1[0] - cnt0[0]
     t_a = (ms1[0] - ms0[0]) / max(na, 1)
-    bytes_a = (hi - lo) * int(np.prod(cfg.dims[:-1])) * esize
+    j_local = (hi - lo) * int(np.prod(cfg.dims[:-1]))
+    bytes_a = j_local * esize
     achieved = bytes_a / (t_a * 1e-3) / 1e9 if t_a > 0 else 0.0
     traffic = None
     prof_json = ROOT / "profiles" / "pass_a_traffic.json"
@@ -269,65 +339,80 @@ def main():
             traffic = None
     impl = eng.pass_impl()
     kname = {_native.PASS_OZAKI: "k_oz_pass<0>: pass A (MTTKRP modes 1..N-1 + trial-fit contraction) on the int8 "
-                                 "tensor cores, exact 8-digit split of the fp64 operands (tcgen05 kind::i8)",
+                                 "tensor cores, 8-plane digit split of the fp64 operands (Ozaki scheme, tcgen05 "
+                                 "kind::i8; accuracy-guarded, fp64 fallback)",
              _native.PASS_DMMA: "k_pass_dmma<NT,0>: pass A (MTTKRP modes 1..N-1 + trial-fit contraction) on the "
                                 "fp64 tensor cores (DMMA)",
              _native.PASS_FMA: "k_pass_a2: pass A (MTTKRP modes 1..N-1 + trial-fit contraction), fp64 FMA"}[impl]
+    phase_ms = {k: round((ms1[i] - ms0[i]) / np_done, 4) for i, k in enumerate(["pass_a", "pass_b", "lu", "solve"])}
+    # core system: LU with partial pivoting (2/3 n^3) + the explicit inverse of both triangles
+    # (2/3 n^3) when the engine forms it (n_B <= 2560), once per iteration; solves: 3 B-applications
+    # of 2 triangular mat-vecs (2 n^2 flop each) -- real flops, x4 for complex
+    n_b = len(cfg.dims) * cfg.rank ** 2
+    cw = 4.0 if cfg.complex_ else 1.0
+    inv = n_b <= 2560
+    lu_flops = cw * ((2.0 / 3.0) + ((2.0 / 3.0) if inv else 0.0)) * n_b ** 3
+    solve_flops = cw * 3 * 2 * 2.0 * n_b ** 2
+    fp64 = {"dmma_tflops": 37.2, "source": "profiles/r01_fp64_peaks.json (tools/microbench/fp64_peaks.cu)"}
+    try:
+        fp64 = {"dmma_tflops": json.loads((ROOT / "profiles" / "r01_fp64_peaks.json").read_text())["dmma_tflops"],
+                "source": fp64["source"]}
+    except Exception:
+        pass
+    step_bytes = j_local * esize * (1.0 + accepted / max(iters_done, 1))
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
                 "kernel": kname,
                 "bytes_per_launch": bytes_a, "avg_launch_ms": round(t_a, 4), "launches": na,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})",
-                "share_of_step": round(((ms1[0] - ms0[0]) / np_done) / (ms / max(iters_done, 1)), 4) if ms > 0 else None,
-                "phase_ms_per_step": {k: round((ms1[i] - ms0[i]) / np_done, 4)
-                                      for i, k in enumerate(["pass_a", "pass_b", "lu", "solve"])},
-                "phase_note": f"CUDA events around each phase over {np_done} eagerly launched iterations after the timed region"}
+                "share_of_step": round(((ms1[0] - ms0[0]) / np_done) / ms_step, 4) if ms > 0 else None,
+                "phase_ms_per_step": phase_ms,
+                "phase_note": f"CUDA events around each phase over {np_done} eagerly launched iterations after the timed region",
+                "phases": {
+                    "lu": {"bound": "fp64 (DMMA)", "n_B": n_b, "flop_per_step": lu_flops,
+                           "what": "LU with partial pivoting of Phi" + (" + explicit inv(L), inv(U)" if inv else ""),
+                           "achieved_tflops": round(lu_flops / (phase_ms["lu"] * 1e-3) / 1e12, 3) if phase_ms["lu"] > 0 else None,
+                           "peak_tflops": fp64["dmma_tflops"], "peak_source": fp64["source"],
+                           "frac": round(lu_flops / (phase_ms["lu"] * 1e-3) / 1e12 / fp64["dmma_tflops"], 4) if phase_ms["lu"] > 0 else None},
+                    "solve": {"bound": "L2 (Phi^-1 resident)", "flop_per_step": solve_flops,
+                              "achieved_tflops": round(solve_flops / (phase_ms["solve"] * 1e-3) / 1e12, 4) if phase_ms["solve"] > 0 else None,
+                              "frac": round(solve_flops / (phase_ms["solve"] * 1e-3) / 1e12 / fp64["dmma_tflops"], 5) if phase_ms["solve"] > 0 else None},
+                    "step": {"bound": "hbm", "bytes_per_step": step_bytes,
+                             "what": "pass A every step + pass B on accepted steps, J_local * 8 B each",
+                             "hbm_bound_ms": round(step_bytes / (pk["hbm_gbs"] * 1e9) * 1e3, 4),
+                             "frac": round(step_bytes / (pk["hbm_gbs"] * 1e9) * 1e3 / ms_step, 4)}}}
     eng.close()
 
-    # end-to-end through the public API, tensor in pinned host memory
     e2e = None
     if not args.no_e2e:
-        host = torch.empty(y_dev.shape, dtype=y_dev.dtype, pin_memory=True)
-        host.copy_(y_dev)
         del y_dev
         torch.cuda.empty_cache()
-        arr = host.numpy()
-        local_dims = tuple(cfg.dims[:-1]) + (hi - lo,)
-        y_host = np.reshape(arr.T, local_dims, order="F")
-        conf = FitConfig(rank=cfg.rank, variant="auto", tau=tau, tol=0.0, max_iters=K, seed=args.seed, init="random")
-        # process setup, untimed: grow the engine memory pool to the fit's footprint (tensor copy +
-        # digit-plane images + workspace), so the timed call reuses memory instead of mapping it
-        _native.pool_reserve(local, 4 * y_host.nbytes + (2 << 30))
-        if dist:
-            dist.barrier()
-        t0 = time.perf_counter()
-        res = fit(y_host, conf, device=local, distributed=ctx, slab_of=cfg.dims[-1])
-        t1 = time.perf_counter()
-        wall = t1 - t0
-        if dist:
-            t = torch.tensor([wall], device=f"cuda:{local}", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            wall = float(t.item())
-        rt = cfg.rank * sum(cfg.dims)
-        e2e = {"value": res.iters / wall, "unit": UNIT,
+        run_e2e("warm")
+        v_warm, res = e2e_runs["warm"]
+        v_cold = e2e_runs["cold"][0]
+        e2e = {"value": v_warm, "unit": UNIT,
                "h2d_bytes_per_step": int(y_host.nbytes // max(res.iters, 1)),
                "d2h_bytes_per_step": int(rt * esize // max(res.iters, 1)),
+               "cold_value": v_cold,
                "what": "public fit() from pinned host memory: H2D of the tensor slab, preamble, "
-                       f"{res.iters} iterations, factor download; wall clock max over ranks"}
+                       f"{res.iters} iterations, factor download; wall clock max over ranks.  value: a process "
+                       "whose engine memory pool already holds the fit's footprint (an earlier fit); cold_value: "
+                       "the first fit() of the process (pool grows by the tensor + int8 images inside the call)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, desc, cores = run_cpu_reference(cfg, args.seed, 2, warmup=1)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc}
+        r = run_cpu_reference(cfg, args.seed, 3, 1)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port", "sample": r["sample"],
+               "sample_value": r["sample_it_s"], "host": r["host"]}
 
     if rank == 0:
         line({"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": iters_done,
-              "warmup": W, "ms_per_step": round(ms / max(iters_done, 1), 4), "higher_is_better": True,
+              "warmup": W, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
               "scaling": "strong", "vs_baseline": None, "dtype": "f64" if not cfg.complex_ else "c128",
               "data": "synthetic (seeded congruence construction, SURVEY App. B; device-generated)",
               "config": config_desc, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
               "cpu_baseline": cpu, "clocks": clocks,
-              "accepted_in_timed": None})
+              "accepted_in_timed": accepted, "pass_guard": {"fallbacks": fallbacks, "tensor_rejected": guarded}})
     if dist:
         dist.destroy_process_group()
 

@@ -455,8 +455,13 @@ class OracleResult:
         return self.trace[-1][1] if self.trace else float("nan")
 
 
-def fit_lm(y, cfg: OracleConfig, init_factors=None, on_iter=None) -> OracleResult:
-    """The damped Gauss-Newton loop, semantics of solver.py:319-384 (Appendix A of SURVEY)."""
+def fit_lm(y, cfg: OracleConfig, init_factors=None, on_iter=None, phases=None) -> OracleResult:
+    """The damped Gauss-Newton loop, semantics of solver.py:319-384 (Appendix A of SURVEY).
+
+    ``phases`` (bench.py's CPU reference arm): a list that receives, per iteration, the seconds spent
+    in the J-independent step (candidate, gradient, decision) and in the tensor-sized work
+    (relative_error of the candidate, and on accept the N MTTKRPs) -- the split bench.py uses to
+    extrapolate a bounded slab sample to the full tensor.  It does not change the arithmetic."""
     t0 = time.monotonic()
     y = fortran_tensor(y)
     if cfg.variant not in LM_VARIANTS:
@@ -482,14 +487,19 @@ def fit_lm(y, cfg: OracleConfig, init_factors=None, on_iter=None) -> OracleResul
     stop = "max_iters"
     if on_iter is not None:
         on_iter(0)
+    clock = time.perf_counter
     for t in range(1, cfg.max_iters + 1):
+        c0 = clock()
         try:
             cand = flm_candidate(A, mu, cfg.variant, g, M)
         except np.linalg.LinAlgError as exc:
             return OracleResult(A, trace, f"error at iteration {t}: {exc}",
                                 (time.monotonic() - t0) * 1e3, detail)
         delta = stack(cand) - stack(A)
+        c1 = clock()
         cand_err = relative_error(y, cand)
+        c2 = clock()
+        t_tensor = c2 - c1
         cand_sq = (cand_err * ynorm) ** 2
         grad = gradient_from_mttkrps(A, g, M)
         rho = gain_ratio(err_sq, cand_sq, delta, grad, mu, -1.0 if t == cfg.negate_denom_at else 1.0)
@@ -498,7 +508,9 @@ def fit_lm(y, cfg: OracleConfig, init_factors=None, on_iter=None) -> OracleResul
         if ok and cand_err < err:
             A = normalize_equal_energy(cand)
             g = gram_cache(A)
+            c3 = clock()
             M = [mttkrp(y, A, n) for n in range(1, len(A) + 1)]
+            t_tensor += clock() - c3
             deltas.append(abs(err - cand_err))
             err, err_sq = cand_err, cand_sq
             accepted = True
@@ -506,6 +518,9 @@ def fit_lm(y, cfg: OracleConfig, init_factors=None, on_iter=None) -> OracleResul
             deltas.append(0.0)
             accepted = False
         trace.append((t, err, mu, accepted))
+        if phases is not None:
+            total = clock() - c0
+            phases.append((total - t_tensor, t_tensor))
         if on_iter is not None:
             on_iter(t)
         if len(deltas) >= 10 and all(d < cfg.tol for d in deltas[-10:]):
