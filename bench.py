@@ -63,19 +63,46 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+    """nvidia-smi clocks / throttle reasons sampled every 20 ms around the timed region.  nvidia-smi
+    needs ~0.5 s to start, longer than a 20-step timed region, so the sampler is started first and
+    the timed region begins once it is producing rows; rows are stamped with the host clock when
+    read, and the ones inside [begin, end] of the timed region (widened by one sampling period)
+    are the reported samples (``samples_in_window``)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    PERIOD_MS = 20
 
     def __init__(self, index: int):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        import threading
+
+        self.rows = []
+        self.t_begin = self.t_end = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "50"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
         except Exception:
             self.p = None
+            return
+        self.th = threading.Thread(target=self._reader, daemon=True)
+        self.th.start()
+        t0 = time.perf_counter()
+        while not self.rows and time.perf_counter() - t0 < 10.0 and self.p.poll() is None:
+            time.sleep(0.01)
+
+    def _reader(self):
+        for line in self.p.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append((time.perf_counter(), parts))
+
+    def begin(self):
+        self.t_begin = time.perf_counter()
+
+    def end(self):
+        self.t_end = time.perf_counter()
+        time.sleep(2.5 * self.PERIOD_MS / 1e3)  # let the row covering the region's end arrive
 
     def stop(self):
         if self.p is not None:
@@ -84,20 +111,22 @@ class ClockSampler:
                 self.p.wait(timeout=5)
             except Exception:
                 self.p.kill()
-        self.f.flush()
-        rows = []
-        for line in Path(self.f.name).read_text().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                rows.append(parts)
-        os.unlink(self.f.name)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+            self.th.join(timeout=2)
+        rows = [r for _, r in self.rows]
+        if self.t_begin is not None and self.t_end is not None:
+            pad = 1.5 * self.PERIOD_MS / 1e3
+            win = [r for t, r in self.rows if self.t_begin - pad <= t <= self.t_end + pad]
+        else:
+            win = rows
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0,
+                    "samples_in_window": 0, "samples_total": len(rows)}
+        sm = [float(r[0]) for r in win if r[0].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][1]),
-                "reasons": reasons, "samples": len(rows)}
+        reasons = sorted({names[i] for r in win for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(win[0][1]),
+                "reasons": reasons, "samples": len(win), "samples_in_window": len(win),
+                "samples_total": len(rows), "period_ms": self.PERIOD_MS}
 
 
 # ----------------------------------------------------------------------------------------------
@@ -296,10 +325,12 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler.begin()
     ev0.record(stream)
     st = eng.fit_step(K)
     ev1.record(stream)
     torch.cuda.synchronize()
+    sampler.end()
     if dist:
         dist.barrier()
     clocks = sampler.stop()

@@ -136,6 +136,22 @@ int cpf_engine_relative_error(cpf_engine* e, double* out);            /* ||Y-X||
 int cpf_engine_flm_step(cpf_engine* e, double mu, int variant, int refine_steps, void* cand_stacked,
                         int* err_code);
 
+/* ALS baselines (solver.py:294-316 _fit_als; kruskal.py:257-293 als_step / als_line_search_step).
+ * One step of the bound factors at iteration t (1-based): a sweep in ascending mode order, each
+ * mode A_n = M_n pinv_psd(Gamma^(n))^T at the partially updated factors (one tensor read per
+ * mode).  line_search != 0 (variant "als-ls") then scores A_prev + s (A_als - A_prev) for
+ * s in {1.1, t^(1/3)} against the sweep by relative error and keeps the best (strictly smaller
+ * wins, the sweep on ties).  The history A_prev is the iterate the previous call started from --
+ * none right after cpf_engine_set_factors, so the first step is a plain sweep as in the reference
+ * -- or the one given to cpf_engine_set_history (NULL clears it).  *relerr = ||Y - X|| / ||Y|| of
+ * the new factors (the value _fit_als records).  Rank <= 64. */
+int cpf_engine_als_step(cpf_engine* e, int line_search, int t, double* relerr);
+int cpf_engine_set_history(cpf_engine* e, const void* stacked);
+/* pinv_psd(gamma) (kruskal.py:245-254) of a Hermitian PSD R x R matrix (column-major, lower
+ * triangle read) on `device`: Jacobi eigen-decomposition, eigenvalues <= eps R max(w) dropped.
+ * Host buffers in and out; R <= 64. */
+int cpf_pinv_psd(int device, int kind, int R, const void* gram, void* out);
+
 /* Per-phase device time accumulated with CUDA events on the engine stream (profiling on/off).
  * Phases: 0 pass A, 1 pass B, 2 LU factor, 3 solves, 4 other; counts = launches per phase. */
 int cpf_engine_profile(cpf_engine* e, int enable);

@@ -533,6 +533,76 @@ def fit_lm(y, cfg: OracleConfig, init_factors=None, on_iter=None, phases=None) -
 
 
 # ----------------------------------------------------------------------------
+# ALS baselines (kruskal.py:245-293, solver.py:294-316)
+# ----------------------------------------------------------------------------
+
+def pinv_psd(gamma: np.ndarray) -> np.ndarray:
+    """Eigen-decomposition pseudo-inverse, eigenvalues <= eps R lambda_max dropped (kruskal.py:245-254)."""
+    w, v = np.linalg.eigh(gamma)
+    r = gamma.shape[0]
+    cutoff = np.finfo(np.float64).eps * r * max(w.max(initial=0.0), 0.0)
+    inv_w = np.where(w > cutoff, 1.0 / np.where(w > cutoff, w, 1.0), 0.0)
+    return (v * inv_w[None, :]) @ v.conj().T
+
+
+def als_step(y: np.ndarray, factors) -> list:
+    """One sweep in ascending mode order, A_n = M_n pinv_psd(Gamma^(n))^T (kruskal.py:257-265)."""
+    out = [np.asarray(a).copy() for a in factors]
+    for n in range(len(out)):
+        g = gram_cache(out)
+        out[n] = mttkrp(y, out, n + 1) @ pinv_psd(g.excl[n]).T
+    return out
+
+
+def als_line_search_step(y: np.ndarray, factors, history, t: int = 1) -> list:
+    """Sweep, then A_prev + s (A_als - A_prev) for s in {1.1, t^(1/3)}, best relative error
+    (kruskal.py:268-293); plain sweep without history."""
+    stepped = als_step(y, factors)
+    if history is None:
+        return stepped
+    best, best_err = stepped, relative_error(y, stepped)
+    for s in (1.1, float(t) ** (1.0 / 3.0)):
+        cand = [hp + s * (ha - hp) for hp, ha in zip(history, stepped)]
+        err = relative_error(y, cand)
+        if err < best_err:
+            best, best_err = cand, err
+    return best
+
+
+def fit_als(y, cfg: "OracleConfig", init_factors=None) -> "OracleResult":
+    """_fit_als (solver.py:294-316): relative error recorded per sweep, mu = 0, every step
+    "accepted"; stop on the 10-delta tolerance window."""
+    t0 = time.monotonic()
+    y = fortran_tensor(y)
+    rng = np.random.default_rng([cfg.seed, 0])
+    if init_factors is not None:
+        model = [np.array(a, copy=True) for a in init_factors]
+    elif cfg.init == "random":
+        model = random_init(y.shape, cfg.rank, rng, np.iscomplexobj(y))
+    else:
+        raise ValueError(f"oracle supports init='random' only, got {cfg.init!r}")
+    err = relative_error(y, model)
+    trace, deltas = [], []
+    history = None
+    stop = "max_iters"
+    for t in range(1, cfg.max_iters + 1):
+        prev = model
+        if cfg.variant == "als-ls":
+            model = als_line_search_step(y, model, history, t)
+        else:
+            model = als_step(y, model)
+        history = prev
+        new_err = relative_error(y, model)
+        trace.append((t, new_err, 0.0, True))
+        deltas.append(abs(err - new_err))
+        err = new_err
+        if len(deltas) >= 10 and all(d < cfg.tol for d in deltas[-10:]):
+            stop = "tol"
+            break
+    return OracleResult(model, trace, stop, (time.monotonic() - t0) * 1e3, [])
+
+
+# ----------------------------------------------------------------------------
 # Dense dGN oracle (hessian.py:46-60, 122-148, 175-182) for step equivalence
 # ----------------------------------------------------------------------------
 

@@ -63,6 +63,9 @@ ERR_MESSAGE = {
 
 EXPORTED_SYMBOLS = (
     "cpf_abi_version",
+    "cpf_engine_als_step",
+    "cpf_engine_set_history",
+    "cpf_pinv_psd",
     "cpf_device_count",
     "cpf_nccl_unique_id",
     "cpf_engine_create",
@@ -137,6 +140,9 @@ def _declare(lib) -> None:
         "cpf_engine_pass_guard": (I, [P, ctypes.POINTER(I64), ctypes.POINTER(I)]),
         "cpf_engine_load_cptn": (I, [P, ctypes.c_char_p, I64]),
         "cpf_pool_reserve": (I, [I, I64]),
+        "cpf_engine_als_step": (I, [P, I, I, ctypes.POINTER(D)]),
+        "cpf_engine_set_history": (I, [P, P]),
+        "cpf_pinv_psd": (I, [I, I, I, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -181,6 +187,23 @@ def nccl_unique_id() -> bytes:
     if rc != CPF_OK:
         raise NativeError("ncclGetUniqueId failed")
     return buf.raw
+
+
+def pinv_psd(gamma: np.ndarray, device: int = 0) -> np.ndarray:
+    """pinv_psd (kruskal.py:245-254) of a Hermitian PSD R x R matrix on the GPU (cpf_pinv_psd)."""
+    g = np.asarray(gamma)
+    if g.ndim != 2 or g.shape[0] != g.shape[1]:
+        raise ValueError("pinv_psd needs a square matrix")
+    kind = CPF_COMPLEX if np.iscomplexobj(g) else CPF_REAL
+    dt = np.complex128 if kind == CPF_COMPLEX else np.float64
+    gf = np.asfortranarray(g, dtype=dt)
+    out = np.empty(g.shape, dtype=dt, order="F")
+    rc = load().cpf_pinv_psd(int(device), kind, g.shape[0], gf.ctypes.data, out.ctypes.data)
+    if rc == CPF_E_ARG:
+        raise ValueError(f"not supported on the B200 backend: pinv_psd of a {g.shape[0]} x {g.shape[0]} matrix (R <= 64)")
+    if rc != CPF_OK:
+        raise NativeError(f"cpf_pinv_psd failed ({rc})")
+    return out
 
 
 def _raise_for(rc: int, msg: str):
@@ -312,6 +335,18 @@ class Engine:
         self._check(self._lib.cpf_engine_flm_step(self._h, float(mu), VARIANT_CODE[variant], int(refine_steps),
                                                   out.ctypes.data, ctypes.byref(code)))
         return out, code.value
+
+    def als_step(self, line_search: bool, t: int) -> float:
+        v = ctypes.c_double()
+        self._check(self._lib.cpf_engine_als_step(self._h, 1 if line_search else 0, int(t), ctypes.byref(v)))
+        return v.value
+
+    def set_history(self, stacked: np.ndarray | None):
+        if stacked is None:
+            self._check(self._lib.cpf_engine_set_history(self._h, None))
+            return
+        v = np.ascontiguousarray(stacked, dtype=self.dtype)
+        self._check(self._lib.cpf_engine_set_history(self._h, v.ctypes.data))
 
     # -- profiling
     def profile(self, on: bool):

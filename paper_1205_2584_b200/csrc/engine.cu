@@ -42,6 +42,7 @@ struct ApiError : std::runtime_error {
 #include "tensor_pass2.cuh"
 #include "tensor_pass_dmma.cuh"
 #include "tensor_pass_oz.cuh"
+#include "als.cuh"
 
 #define NCCL_CHECK(expr)                                                                   \
   do {                                                                                     \
@@ -82,6 +83,8 @@ struct EngineBase {
   virtual int pass_impl() const = 0;
   virtual void pass_guard(int64_t* fallbacks, int* rejected) = 0;
   virtual void unfolding_gram(int mode, void* out) = 0;
+  virtual double als_step(int line_search, int t) = 0;
+  virtual void set_history(const void* p) = 0;
 };
 
 template <class T>
@@ -298,7 +301,7 @@ struct Engine final : EngineBase {
                     wvec, fvec, xvec, Phi, A1c, KMc, WNc, A1r, KMr, WNr, zpart, m1part, bpart, pa_out, pb_out, pb_all,
                     norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL, WNd, KMd, gring, PhiInv, TriTmp, yvec, tmv_part,
                     ozYA, ozYB, ozBA, ozBB, ozFrowA, ozFrowB, ozFr, ozM1, ozZ, ozBp,
-                    PhiS, PhiInvS, TriTmpS, GtiS, GiS, invLS, ibufS, gringS, spec_sing};
+                    PhiS, PhiInvS, TriTmpS, GtiS, GiS, invLS, ibufS, gringS, spec_sing, Hist, Pinv};
     for (void* p : ptrs)
       if (p) cudaFreeAsync(p, s);  // back to the device pool (kept for the next engine)
     if (hst) cudaFreeHost(hst);
@@ -1509,6 +1512,7 @@ struct Engine final : EngineBase {
     }
     oz_split();
     have_tensor = true;
+    ysq_cached = -1.0;
   }
   // CPTN file -> this rank's slab in device memory, double-buffered through pinned staging
   void load_cptn(const char* path, int64_t payload_off) override {
@@ -1561,10 +1565,12 @@ struct Engine final : EngineBase {
     Y = Yown;
     oz_split();
     have_tensor = true;
+    ysq_cached = -1.0;
   }
   void set_factors(const void* p) override {
     CPF_CUDA_CHECK(cudaMemcpyAsync(A, p, RT * sizeof(T), cudaMemcpyHostToDevice, s));
     have_factors = true;
+    have_hist = false;
   }
   void get_factors(void* p) override {
     CPF_CUDA_CHECK(cudaMemcpyAsync(p, A, RT * sizeof(T), cudaMemcpyDeviceToHost, s));
@@ -1910,6 +1916,81 @@ struct Engine final : EngineBase {
     cudaFree(part);
     cudaFree(G);
   }
+
+  // ------------------------------------------------------------------------------------------
+  // ALS / ALS with line search (solver.py:294-316, kruskal.py:245-293) on the engine's kernels:
+  // one MTTKRP per mode per sweep through pass A (modes 1..N-1) / pass B (mode N) at the
+  // partially updated factors, the Gram cache, pinv_psd by Jacobi (als.cuh), A_n = M_n pinv^T.
+  // ------------------------------------------------------------------------------------------
+  T* Hist = nullptr;   // previous iterate (history of the line search)
+  T* Pinv = nullptr;   // R x R
+  bool have_hist = false, pinv_attr = false;
+  double ysq_cached = -1.0;
+
+  void als_alloc() {
+    if (R > kPinvMaxR) throw ApiError(CPF_E_UNSUPPORTED, "ALS: rank > 64 is outside the pinv_psd kernel");
+    if (!Hist) Hist = dalloc<T>(RT);
+    if (!Pinv) Pinv = dalloc<T>((size_t)R * R);
+    if (!pinv_attr) {
+      CPF_CUDA_CHECK(cudaFuncSetAttribute(k_pinv_psd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)pinv_smem_bytes<T>(kPinvMaxR)));
+      pinv_attr = true;
+    }
+  }
+  // one ALS sweep of F in place (kruskal.py:257-265)
+  void als_sweep(T* F) {
+    for (int n = 0; n < N; ++n) {
+      if (n < N - 1) pass_a(F, M, kAlways);
+      else pass_b(F, M, kAlways);
+      cross_gram(F, F, Cg, kAlways);
+      cache_from_grams(Cg, kAlways);
+      launch(k_pinv_psd<T>, 1, 256, pinv_smem_bytes<T>(R), (const T*)(Gx + (size_t)n * R * R), R, Pinv);
+      launch(k_als_factor<T>, nblocks(dims[n] * R, 128), 128, (size_t)R * R * sizeof(T), (const T*)(M + offs[n]),
+             (const T*)Pinv, dims[n], R, F + offs[n]);
+    }
+  }
+  double relerr_of(const T* F) {
+    if (ysq_cached < 0.0) ysq_cached = ynorm_sq();
+    if (ysq_cached == 0.0) throw ApiError(CPF_E_ZERODIV, "relative error undefined for a zero tensor");
+    direct_resid(F, dscal + 5, kAlways);
+    double res;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(&res, dscal + 5, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    return std::sqrt(res) / std::sqrt(ysq_cached);
+  }
+  // One ALS (line_search = 0) or ALS-ls step of the bound factors A at iteration t; the history is
+  // the iterate before the previous call (none right after set_factors) or set_history's.
+  double als_step(int line_search, int t) override {
+    require_ready();
+    als_alloc();
+    reset_state(0, 0.0, 0.0, 0);
+    CPF_CUDA_CHECK(cudaMemcpyAsync(Cand, A, RT * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    als_sweep(Cand);
+    const T* best = Cand;
+    double err = -1.0;
+    if (line_search && have_hist) {  // kruskal.py:279-292
+      err = relerr_of(Cand);
+      const double steps[2] = {1.1, std::pow((double)t, 1.0 / 3.0)};
+      T* bufs[2] = {V1, V2};
+      for (int k = 0; k < 2; ++k) {
+        launch(k_als_extrap<T>, nblocks(RT, 256), 256, 0, (const T*)Hist, (const T*)Cand, steps[k], RT, bufs[k]);
+        const double e2 = relerr_of(bufs[k]);
+        if (e2 < err) { best = bufs[k]; err = e2; }
+      }
+    }
+    CPF_CUDA_CHECK(cudaMemcpyAsync(Hist, A, RT * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    have_hist = true;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(A, best, RT * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    if (err < 0.0) err = relerr_of(A);
+    return err;
+  }
+  void set_history(const void* p) override {
+    als_alloc();
+    if (!p) { have_hist = false; return; }
+    CPF_CUDA_CHECK(cudaMemcpyAsync(Hist, p, RT * sizeof(T), cudaMemcpyHostToDevice, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    have_hist = true;
+  }
 };
 
 }  // namespace cpf
@@ -2059,6 +2140,47 @@ int cpf_engine_trace(cpf_engine* e, cpf_iter_record* out, int cap, int* n) {
 int cpf_engine_mttkrp(cpf_engine* e, int mode, void* out) {
   if (!e || !e->impl) return CPF_E_STATE;
   return guarded(e, [&] { e->impl->mttkrp(mode, out); });
+}
+
+int cpf_pinv_psd(int device, int kind, int R, const void* gram, void* out) {
+  if (R < 1 || R > kPinvMaxR || !gram || !out) return CPF_E_ARG;
+  if (kind != CPF_REAL && kind != CPF_COMPLEX) return CPF_E_KIND;
+  const size_t es = kind == CPF_COMPLEX ? 16 : 8;
+  const size_t bytes = es * (size_t)R * R;
+  void *dg = nullptr, *dout = nullptr;
+  cudaError_t rc = cudaSetDevice(device);
+  if (rc == cudaSuccess) rc = cudaMalloc(&dg, bytes);
+  if (rc == cudaSuccess) rc = cudaMalloc(&dout, bytes);
+  if (rc == cudaSuccess) rc = cudaMemcpy(dg, gram, bytes, cudaMemcpyHostToDevice);
+  if (rc == cudaSuccess) {
+    if (kind == CPF_COMPLEX) {
+      rc = cudaFuncSetAttribute(k_pinv_psd<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pinv_smem_bytes<cplx>(kPinvMaxR));
+      if (rc == cudaSuccess) k_pinv_psd<cplx><<<1, 256, pinv_smem_bytes<cplx>(R)>>>((const cplx*)dg, R, (cplx*)dout);
+    } else {
+      rc = cudaFuncSetAttribute(k_pinv_psd<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pinv_smem_bytes<double>(kPinvMaxR));
+      if (rc == cudaSuccess) k_pinv_psd<double><<<1, 256, pinv_smem_bytes<double>(R)>>>((const double*)dg, R, (double*)dout);
+    }
+    if (rc == cudaSuccess) rc = cudaGetLastError();
+  }
+  if (rc == cudaSuccess) rc = cudaMemcpy(out, dout, bytes, cudaMemcpyDeviceToHost);
+  if (dg) cudaFree(dg);
+  if (dout) cudaFree(dout);
+  return rc == cudaSuccess ? CPF_OK : CPF_E_CUDA;
+}
+
+int cpf_engine_als_step(cpf_engine* e, int line_search, int t, double* relerr) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] {
+    const double v = e->impl->als_step(line_search, t);
+    if (relerr) *relerr = v;
+  });
+}
+
+int cpf_engine_set_history(cpf_engine* e, const void* stacked) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->set_history(stacked); });
 }
 
 int cpf_engine_relative_error(cpf_engine* e, double* out) {

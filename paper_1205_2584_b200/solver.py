@@ -215,16 +215,56 @@ def _make_engine(y: DenseTensor, rank: int, device, distributed, slab_of=None):
     return eng
 
 
+ALS_VARIANTS = ("als", "als-ls")
+
+
 def _check_lm(config: FitConfig):
-    if config.variant not in LM_VARIANTS:
+    if config.variant not in LM_VARIANTS + ALS_VARIANTS:
         raise ValueError(f"variant {config.variant!r} is not supported on the B200 backend "
-                         "(only the fast damped Gauss-Newton variants 'auto', 'flm-a', 'flm-b')")
+                         "(the fast damped Gauss-Newton variants 'auto', 'flm-a', 'flm-b' and the "
+                         "ALS baselines 'als', 'als-ls')")
     if config.init not in ("svd", "random"):
         raise ValueError(f"unknown init {config.init!r}")
 
 
+def _stop_on_tol(err_deltas, tol) -> bool:
+    """solver.py:274-275."""
+    return len(err_deltas) >= 10 and all(d < tol for d in err_deltas[-10:])
+
+
+def _run_als(eng, gdims, scalar_kind: str, config: FitConfig, rng) -> FitResult:
+    """_fit_als (solver.py:294-316) on an engine whose tensor is bound: every sweep, line search
+    and relative error runs on the device (cpf_engine_als_step); the host keeps the reference's
+    10-delta tolerance window.  Closes the engine."""
+    try:
+        init = _init_model(_Dims(gdims, scalar_kind), config, rng, eng)
+        eng.set_factors(init.as_vector())
+        err = eng.relative_error()
+        trace, deltas = [], []
+        stop_reason = "max_iters"
+        line_search = config.variant == "als-ls"
+        for t in range(1, config.max_iters + 1):
+            new_err = eng.als_step(line_search, t)
+            trace.append(IterRecord(t, new_err, 0.0, True))
+            deltas.append(abs(err - new_err))
+            err = new_err
+            if _stop_on_tol(deltas, config.tol):
+                stop_reason = "tol"
+                break
+        model = model_from_vector(eng.get_factors(), gdims, config.rank)
+        fallbacks, rejected = eng.pass_guard()
+        result = FitResult(model, trace, stop_reason, launches=eng.launch_count(), pass_impl=eng.pass_impl(),
+                           pass_fallbacks=fallbacks, tensor_guarded=rejected)
+    finally:
+        eng.close()
+    return result
+
+
 def _run_fit(eng, gdims, scalar_kind: str, config: FitConfig, rng) -> FitResult:
-    """The LM loop on an engine whose tensor is bound (solver.py:319-384); closes the engine."""
+    """The LM loop on an engine whose tensor is bound (solver.py:319-384); closes the engine.
+    ALS variants go to _run_als (solver.py:285-288 dispatch)."""
+    if config.variant in ALS_VARIANTS:
+        return _run_als(eng, gdims, scalar_kind, config, rng)
     try:
         tt = [time.monotonic()]
         init = _init_model(_Dims(gdims, scalar_kind), config, rng, eng)
@@ -382,6 +422,43 @@ def flm_step(y, model, mu: float, variant: str = "auto", cache=None, mttkrps=Non
         if code in (_native.ERR_KERNEL_SINGULAR, _native.ERR_PHI1_SINGULAR):
             raise SingularKernelError(_native.ERR_MESSAGE[code])
         raise np.linalg.LinAlgError(_native.ERR_MESSAGE.get(code, "numerical error"))
+    return model_from_vector(vec, model.dims, model.rank)
+
+
+def pinv_psd(gamma, *, device=None) -> np.ndarray:
+    """Pseudo-inverse of a Hermitian PSD matrix (kruskal.py:245-254) on the GPU: Jacobi
+    eigen-decomposition, eigenvalues below eps * R * lambda_max truncated."""
+    return _native.pinv_psd(gamma, 0 if device is None else int(device))
+
+
+def als_step(y, model, *, device=None) -> KruskalModel:
+    """One ALS sweep, factors updated in ascending mode order (kruskal.py:257-265)."""
+    y, model = as_dense(y), as_model(model)
+    eng = _model_engine(y, model, device)
+    try:
+        eng.als_step(False, 1)
+        vec = eng.get_factors()
+    finally:
+        eng.close()
+    return model_from_vector(vec, model.dims, model.rank)
+
+
+def als_line_search_step(y, model, history, t: int = 1, *, device=None) -> KruskalModel:
+    """ALS sweep with extrapolation against the previous iterate (kruskal.py:268-293): candidates
+    A_prev + s (A_als - A_prev), s in {1.1, t^(1/3)}, scored by relative error; plain ALS when
+    ``history`` is None."""
+    y, model = as_dense(y), as_model(model)
+    eng = _model_engine(y, model, device)
+    try:
+        if history is not None:
+            history = as_model(history)
+            dtype = np.complex128 if np.iscomplexobj(y.data) else np.float64
+            eng.set_history(np.concatenate([np.asarray(f, dtype=dtype).reshape(-1, order="F")
+                                            for f in history.factors]))
+        eng.als_step(True, t)
+        vec = eng.get_factors()
+    finally:
+        eng.close()
     return model_from_vector(vec, model.dims, model.rank)
 
 

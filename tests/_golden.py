@@ -68,3 +68,34 @@ def split_stacked(vec, dims, rank):
         out.append(np.asarray(vec[off: off + d * rank]).reshape((d, rank), order="F"))
         off += d * rank
     return out
+
+
+def _grouped(fname: str) -> dict:
+    z = np.load(GOLDEN / fname, allow_pickle=False)
+    out: dict = {}
+    for key in z.files:
+        if "__" not in key:
+            out[key] = z[key]
+            continue
+        cname, field = key.split("__", 1)
+        out.setdefault(cname, {})[field] = z[key]
+    return out
+
+
+def als_fits() -> dict:
+    """ALS / ALS-ls fits captured from the reference (tests/golden/make_als_golden.py)."""
+    return {k: v for k, v in _grouped("als_fits.npz").items() if isinstance(v, dict)}
+
+
+def als_units() -> dict:
+    return _grouped("als_units.npz")
+
+
+def als_config(name: str, case: dict):
+    """SynthConfig of an ALS fit fixture (name = '<config>_<variant>')."""
+    from paper_1205_2584_b200 import synth
+
+    base = name.rsplit("_", 1)[0]
+    key = base.split("_")[0]
+    dims = tuple(int(x) for x in case["dims"])
+    return synth.scaled(synth.CONFIGS[key], dims, rank=int(case["rank"]), max_iters=int(case["max_iters"]), name=base)
