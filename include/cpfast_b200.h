@@ -66,6 +66,8 @@ extern "C" {
 #define CPF_ERR_PHI1_SINGULAR 3    /* SingularKernelError("I + Psi K numerically singular: Singular matrix") */
 #define CPF_ERR_ZERO_COLUMN 4      /* ZeroDivisionError while normalising an accepted candidate */
 #define CPF_ERR_NONFINITE 5
+#define CPF_ERR_KINV_SINGULAR 6    /* SingularKernelError("a pairwise Gamma entry vanishes; K is singular") (hessian.py:97-107) */
+#define CPF_ERR_SBCK_SINGULAR 7    /* SingularKernelError("Sb + Chat K numerically singular: Singular matrix") (hessian.py:266-267) */
 
 typedef struct cpf_engine cpf_engine;
 
@@ -147,6 +149,17 @@ int cpf_engine_flm_step(cpf_engine* e, double mu, int variant, int refine_steps,
  * the new factors (the value _fit_als records).  Rank <= 64. */
 int cpf_engine_als_step(cpf_engine* e, int line_search, int t, double* relerr);
 int cpf_engine_set_history(cpf_engine* e, const void* stacked);
+/* fast_damped_inverse(cache, factors, mu, use_kernel_inverse) (hessian.py:232-277) at the bound
+ * factors (no tensor needed): gamma_tilde = N blocks (Gamma^(n) + mu I)^{-1} (R x R, column-major,
+ * stacked) and the core grid D (N R^2 x N R^2, column-major; block (n, m) is S[n][m]), computed
+ * from the same O(1)-conditioned systems as the reference (K^{-1} path: inv(Sb K~ Sb +
+ * blkdiag((Gamma_n + mu I) kron C_n)); K-free path: blkdiag(Gt kron I) K inv(Sb + Chat K)) with the
+ * engine's LU and triangular inverses.  use_kernel_inverse: -1 = auto (kernel_is_invertible),
+ * 0 = K-free, 1 = K^{-1}.  mu <= 0 is CPF_E_ARG.  *err_code = CPF_ERR_KINV_SINGULAR (K^{-1}
+ * requested, K singular), CPF_ERR_SBCK_SINGULAR (K-free system singular), CPF_ERR_SINGULAR
+ * (np.linalg.inv failure) or 0. */
+int cpf_engine_fast_damped_inverse(cpf_engine* e, double mu, int use_kernel_inverse, void* gamma_tilde, void* core,
+                                   int* err_code);
 /* pinv_psd(gamma) (kruskal.py:245-254) of a Hermitian PSD R x R matrix (column-major, lower
  * triangle read) on `device`: Jacobi eigen-decomposition, eigenvalues <= eps R max(w) dropped.
  * Host buffers in and out; R <= 64. */

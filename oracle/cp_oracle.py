@@ -281,6 +281,54 @@ def b_core(g: Grams, mu: float, use_kernel_inverse: bool) -> np.ndarray:
         raise OracleSingularKernel(f"I + Psi K numerically singular: {exc}")
 
 
+def fast_damped_inverse(factors, mu: float, use_kernel_inverse=None):
+    """(gamma_tilde list, core grid D) of the structured (H + mu I)^{-1} (hessian.py:232-277):
+    K^{-1} path D = inv(Sb K~ Sb + blkdiag((Gamma_n + mu I) kron C_n)); K-free path
+    D = blkdiag(Gt kron I) K solve(Sb + Chat K, I)."""
+    if mu <= 0:
+        raise ValueError("mu must be positive")
+    g = gram_cache(factors)
+    if use_kernel_inverse is None:
+        use_kernel_inverse = kernel_is_invertible(g)
+    r = g.full.shape[0]
+    eye = np.eye(r)
+    gamma_tilde = [np.linalg.inv(x + mu * eye) for x in g.excl]
+    damped = [g.excl[n] + mu * eye for n in range(len(factors))]
+    sb = scipy.linalg.block_diag(*[np.kron(x, eye) for x in damped])
+    if use_kernel_inverse:
+        diag = scipy.linalg.block_diag(*[np.kron(x, c) for x, c in zip(damped, g.C)])
+        d = np.linalg.inv(sb @ kernel_inverse(g) @ sb + diag)
+    else:
+        chat = scipy.linalg.block_diag(*[np.kron(eye, c) for c in g.C])
+        k = kernel_matrix(g)
+        gt = scipy.linalg.block_diag(*[np.kron(x, eye) for x in gamma_tilde])
+        try:
+            d = gt @ k @ np.linalg.solve(sb + chat @ k, np.eye(k.shape[0]))
+        except np.linalg.LinAlgError as exc:
+            raise OracleSingularKernel(f"Sb + Chat K numerically singular: {exc}")
+    return gamma_tilde, d
+
+
+def materialize_inverse(gamma_tilde, core, factors) -> np.ndarray:
+    """Dense (H + mu I)^{-1} from the block form (hessian.py:278-297; test scaffolding)."""
+    r = gamma_tilde[0].shape[0]
+    r2 = r * r
+    nm = len(factors)
+    eye_r = np.eye(r)
+    rows = []
+    for n in range(nm):
+        row = []
+        for m in range(nm):
+            zn = np.kron(eye_r, factors[n])
+            zm = np.kron(eye_r, factors[m])
+            block = -zn @ core[n * r2:(n + 1) * r2, m * r2:(m + 1) * r2] @ zm.conj().T
+            if n == m:
+                block = block + np.kron(gamma_tilde[n], np.eye(factors[n].shape[0]))
+            row.append(block)
+        rows.append(row)
+    return np.block(rows)
+
+
 def core_matrix(g: Grams, mu: float, variant: str) -> np.ndarray:
     """Variant dispatch (solver.py:143-148)."""
     if variant == "auto":

@@ -17,11 +17,13 @@ from .solver import (
     FitResult,
     IterRecord,
     SingularKernelError,
+    StructuredInverse,
     als_line_search_step,
     als_step,
     fit,
     fit_complex,
     fit_file,
+    fast_damped_inverse,
     flm_step,
     mttkrp,
     pinv_psd,
@@ -37,4 +39,5 @@ __all__ = [
     "LM_VARIANTS", "MU_OVERFLOW", "VARIANTS", "FitConfig", "FitResult", "IterRecord",
     "SingularKernelError", "fit", "fit_complex", "fit_file", "flm_step", "mttkrp", "random_init",
     "relative_error", "slab_bounds", "ALS_VARIANTS", "als_step", "als_line_search_step", "pinv_psd",
+    "StructuredInverse", "fast_damped_inverse",
 ]

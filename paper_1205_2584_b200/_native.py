@@ -51,6 +51,8 @@ ERR_KERNEL_SINGULAR = 2
 ERR_PHI1_SINGULAR = 3
 ERR_ZERO_COLUMN = 4
 ERR_NONFINITE = 5
+ERR_KINV_SINGULAR = 6
+ERR_SBCK_SINGULAR = 7
 
 # messages of the reference's in-loop exceptions (solver.py:349-352; hessian.py:146-147, 210-211;
 # numpy.linalg "Singular matrix")
@@ -59,12 +61,15 @@ ERR_MESSAGE = {
     ERR_KERNEL_SINGULAR: "flm-b requested but K is singular",
     ERR_PHI1_SINGULAR: "I + Psi K numerically singular: Singular matrix",
     ERR_NONFINITE: "non-finite values in the step",
+    ERR_KINV_SINGULAR: "a pairwise Gamma entry vanishes; K is singular",
+    ERR_SBCK_SINGULAR: "Sb + Chat K numerically singular: Singular matrix",
 }
 
 EXPORTED_SYMBOLS = (
     "cpf_abi_version",
     "cpf_engine_als_step",
     "cpf_engine_set_history",
+    "cpf_engine_fast_damped_inverse",
     "cpf_pinv_psd",
     "cpf_device_count",
     "cpf_nccl_unique_id",
@@ -143,6 +148,7 @@ def _declare(lib) -> None:
         "cpf_engine_als_step": (I, [P, I, I, ctypes.POINTER(D)]),
         "cpf_engine_set_history": (I, [P, P]),
         "cpf_pinv_psd": (I, [I, I, I, P, P]),
+        "cpf_engine_fast_damped_inverse": (I, [P, D, I, P, P, ctypes.POINTER(I)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -340,6 +346,18 @@ class Engine:
         v = ctypes.c_double()
         self._check(self._lib.cpf_engine_als_step(self._h, 1 if line_search else 0, int(t), ctypes.byref(v)))
         return v.value
+
+    def fast_damped_inverse(self, mu: float, use_kernel_inverse):
+        """(gamma_tilde (N, R, R), core grid D (N R^2 x N R^2), CPF_ERR_* code)."""
+        n, r = len(self.dims), self.rank
+        nb = n * r * r
+        gt = np.empty(n * r * r, dtype=self.dtype)
+        d = np.empty((nb, nb), dtype=self.dtype, order="F")
+        code = ctypes.c_int(0)
+        uk = -1 if use_kernel_inverse is None else (1 if use_kernel_inverse else 0)
+        self._check(self._lib.cpf_engine_fast_damped_inverse(self._h, float(mu), uk, gt.ctypes.data, d.ctypes.data,
+                                                             ctypes.byref(code)))
+        return [gt[k * r * r:(k + 1) * r * r].reshape((r, r), order="F") for k in range(n)], d, code.value
 
     def set_history(self, stacked: np.ndarray | None):
         if stacked is None:

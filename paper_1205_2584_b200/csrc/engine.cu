@@ -43,6 +43,7 @@ struct ApiError : std::runtime_error {
 #include "tensor_pass_dmma.cuh"
 #include "tensor_pass_oz.cuh"
 #include "als.cuh"
+#include "fdi.cuh"
 
 #define NCCL_CHECK(expr)                                                                   \
   do {                                                                                     \
@@ -85,6 +86,7 @@ struct EngineBase {
   virtual void unfolding_gram(int mode, void* out) = 0;
   virtual double als_step(int line_search, int t) = 0;
   virtual void set_history(const void* p) = 0;
+  virtual int fast_damped_inverse(double mu, int use_kinv, void* gt_out, void* d_out) = 0;
 };
 
 template <class T>
@@ -1984,6 +1986,46 @@ struct Engine final : EngineBase {
     if (err < 0.0) err = relerr_of(A);
     return err;
   }
+  // fast_damped_inverse (hessian.py:232-277) at the bound factors: gamma_tilde_n = (Gamma_n + mu I)^-1
+  // (N R x R) and the core grid D (nB x nB), through the engine's Gram cache, LU and substitution
+  // on the identity (fdi.cuh).  use_kinv: -1 auto (kernel_is_invertible), 0 K-free, 1 K^{-1}.  Returns a
+  // CPF_ERR_* code (0 = ok).  Needs factors only (no tensor).
+  int fast_damped_inverse(double mu, int use_kinv, void* gt_out, void* d_out) override {
+    if (!have_factors) throw ApiError(CPF_E_STATE, "no factors bound");
+    if (!(mu > 0.0)) throw ApiError(CPF_E_ARG, "mu must be positive");
+    if (N < 2) throw ApiError(CPF_E_ARG, "kernel inverse needs at least two modes");
+    reset_state(use_kinv < 0 ? 0 : (use_kinv ? 2 : 1), mu, 0.0, 1);
+    cross_gram(A, A, Cg, kAlways);
+    cache_from_grams(Cg, kAlways);
+    int kok = 0;
+    CPF_CUDA_CHECK(cudaMemcpyAsync(&kok, kinv_ok, sizeof(int), cudaMemcpyDeviceToHost, s));
+    pull_state();
+    if (use_kinv == 1 && !kok) return CPF_ERR_KINV_SINGULAR;
+    const int kinv = hst->use_kinv;
+    launch(k_damped_inverses<T>, 2 * N, 128, 2 * R * R * sizeof(T), (const T*)Gx, N, R, Gti, Gi, st, (const DevFlags*)fl,
+           (int)kAlways, (const int*)nullptr, (const double*)nullptr, (int*)nullptr);
+    pull_state();
+    if (hst->err_code) return CPF_ERR_SINGULAR;  // np.linalg.inv(g + mu I) failed
+    launch(k_fdi_assemble<T>, nblocks((int64_t)nB * nB, 256), 256, 0, Phi, N, R, (const T*)Cg, (const T*)Gx,
+           (const T*)Gp, (const T*)Gf, mu, kinv);
+    lu_factor(0);
+    pull_state();
+    if (hst->err_code) return kinv ? CPF_ERR_SINGULAR : CPF_ERR_SBCK_SINGULAR;
+    if (!TriTmp) TriTmp = dalloc<T>((size_t)nB * nB);
+    launch(k_perm_ident<T>, nblocks((int64_t)nB * nB, 256), 256, 0, (const int*)lu.perm, nB, TriTmp);
+    launch(k_trsm_ident<T, true>, nblocks(nB, 16), 256, 0, (const T*)Phi, nB, TriTmp);
+    launch(k_trsm_ident<T, false>, nblocks(nB, 16), 256, 0, (const T*)Phi, nB, TriTmp);
+    const T* Dres = TriTmp;
+    if (!kinv) {
+      launch(k_fdi_gtk<T>, nblocks((int64_t)nB * nB, 256), 256, 0, (const T*)TriTmp, N, R, (const T*)Gi, (const T*)Gp,
+             Phi);
+      Dres = Phi;
+    }
+    CPF_CUDA_CHECK(cudaMemcpyAsync(gt_out, Gi, sizeof(T) * N * R * R, cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaMemcpyAsync(d_out, Dres, sizeof(T) * nB * nB, cudaMemcpyDeviceToHost, s));
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    return 0;
+  }
   void set_history(const void* p) override {
     als_alloc();
     if (!p) { have_hist = false; return; }
@@ -2176,6 +2218,12 @@ int cpf_engine_als_step(cpf_engine* e, int line_search, int t, double* relerr) {
     const double v = e->impl->als_step(line_search, t);
     if (relerr) *relerr = v;
   });
+}
+
+int cpf_engine_fast_damped_inverse(cpf_engine* e, double mu, int use_kernel_inverse, void* gamma_tilde, void* core,
+                                   int* err_code) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { *err_code = e->impl->fast_damped_inverse(mu, use_kernel_inverse, gamma_tilde, core); });
 }
 
 int cpf_engine_set_history(cpf_engine* e, const void* stacked) {

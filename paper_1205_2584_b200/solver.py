@@ -462,5 +462,50 @@ def als_line_search_step(y, model, history, t: int = 1, *, device=None) -> Krusk
     return model_from_vector(vec, model.dims, model.rank)
 
 
+@dataclass
+class StructuredInverse:
+    """Block form of (H + mu I)^{-1} (hessian.py:214-229): gamma_tilde[n] = (Gamma^(n) + mu I)^{-1},
+    S[n][m] the R^2 x R^2 blocks of the core grid."""
+
+    gamma_tilde: list
+    S: list
+    mu: float
+
+    def scalar_count(self) -> int:
+        n = len(self.gamma_tilde)
+        r2 = self.gamma_tilde[0].size
+        return n * r2 + sum(b.size for row in self.S for b in row)
+
+
+def fast_damped_inverse(cache, factors, mu: float, use_kernel_inverse=None, *, device=None) -> StructuredInverse:
+    """Structured (H + mu I)^{-1} from the low-rank adjustment (hessian.py:232-277), on the GPU.
+
+    ``cache`` is accepted for signature compatibility; the engine recomputes the Gram cache from
+    ``factors`` on the device (it is a pure function of them).  ``use_kernel_inverse=None`` picks
+    the explicit-K^{-1} path exactly when the kernel invertibility proxy holds.  Errors as the
+    reference: ValueError for mu <= 0, SingularKernelError for a singular K (K^{-1} path requested)
+    or a singular K-free system, LinAlgError("Singular matrix") otherwise."""
+    if mu <= 0:
+        raise ValueError("mu must be positive")
+    model = as_model(factors if isinstance(factors, KruskalModel) else KruskalModel(list(factors)))
+    if model.order < 2:
+        raise ValueError("kernel inverse needs at least two modes")
+    kind = _native.CPF_COMPLEX if model.scalar_kind == COMPLEX else _native.CPF_REAL
+    eng = _native.Engine(kind, model.dims, model.rank, 0 if device is None else int(device))
+    try:
+        eng.set_factors(model.as_vector())
+        gt, d, code = eng.fast_damped_inverse(mu, use_kernel_inverse)
+    finally:
+        eng.close()
+    if code in (_native.ERR_KINV_SINGULAR, _native.ERR_SBCK_SINGULAR):
+        raise SingularKernelError(_native.ERR_MESSAGE[code])
+    if code:
+        raise np.linalg.LinAlgError(_native.ERR_MESSAGE.get(code, "numerical error"))
+    r2 = model.rank * model.rank
+    n_modes = model.order
+    S = [[d[n * r2:(n + 1) * r2, m * r2:(m + 1) * r2] for m in range(n_modes)] for n in range(n_modes)]
+    return StructuredInverse(gt, S, mu)
+
+
 class SingularKernelError(np.linalg.LinAlgError):
     """The kernel matrix K is (numerically) singular (hessian.py:34-35)."""
