@@ -195,7 +195,9 @@ struct LmDeviceState {
                              // mu instead and needs a freshly factored core system.
   int test_negdenom_iter;    // test hook (CPF_TEST_NEGDENOM=t): negate the gain-ratio denominator
                              // at iteration t to force a rho > 0 / not-improved rejection
-  int pad_[2];
+  int test_singular_iter;   // test hook (CPF_TEST_SINGULAR=t): zero a column of the core system that
+                            // iteration t factors (fault injection: a zero pivot, solver.py:349-352)
+  int pad_[1];
 };
 
 // Gate of the core-system kernels (Phi, LU, inverse): gate_running 0 = always, 1 = while the fit

@@ -112,6 +112,7 @@ struct Engine final : EngineBase {
   const T* Y = nullptr;
   T* Yown = nullptr;
   bool have_tensor = false, have_factors = false;
+  bool test_singular = false;  // fault-injection kernel in prepare_core (CPF_TEST_SINGULAR)
 
   // ---- device buffers
   T *A = nullptr, *Ac = nullptr, *M = nullptr, *Mc = nullptr, *D = nullptr, *G = nullptr, *Cand = nullptr;
@@ -1379,6 +1380,7 @@ struct Engine final : EngineBase {
     }
     launch(k_phi_assemble<T>, nblocks((int64_t)nB * nB, 256), 256, 0, Phi, N, R, (const T*)Cg, (const T*)Gi,
            (const T*)Gp, (const T*)Gf, (const LmDeviceState*)st, gr);
+    if (test_singular) launch(k_test_zero_col<T>, 1, 256, 0, Phi, nB, (const LmDeviceState*)st, mode == 1 ? 2 : 1);
     mark(5);
     lu_factor(gr);
     mark(6);
@@ -1643,6 +1645,10 @@ struct Engine final : EngineBase {
     hst->rej_grow = 0;
     hst->test_negdenom_iter = 0;
     if (const char* e = getenv("CPF_TEST_NEGDENOM")) hst->test_negdenom_iter = atoi(e);  // test hook
+    hst->test_singular_iter = 0;
+    if (const char* e = getenv("CPF_TEST_SINGULAR")) hst->test_singular_iter = atoi(e);  // test hook
+    if (test_singular != (hst->test_singular_iter != 0) && gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+    test_singular = hst->test_singular_iter != 0;
     // keep use_kinv computed by the cache kernels
     LmDeviceState tmp;
     CPF_CUDA_CHECK(cudaMemcpyAsync(&tmp, st, sizeof(tmp), cudaMemcpyDeviceToHost, s));

@@ -62,6 +62,16 @@ __global__ void k_phi_assemble(T* __restrict__ Phi, int N, int R, const T* __res
   Phi[idx] = v;
 }
 
+// Fault injection (test hook CPF_TEST_SINGULAR=t): zero column 0 of the core system factored for
+// iteration t (offset: 1 for the next step's system, 2 for the speculated rejection branch's) so its
+// LU meets an exactly zero pivot -- the reference's LinAlgError("Singular matrix") stop.
+template <class T>
+__global__ void k_test_zero_col(T* __restrict__ Phi, int nB, const LmDeviceState* st, int offset) {
+  pdl_wait();
+  if (st->test_singular_iter == 0 || st->iter + offset != st->test_singular_iter) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nB; i += gridDim.x * blockDim.x) Phi[i] = zero_of<T>();
+}
+
 // flm-a: f = K z  ((K z)_n[a + R b] = sum_{m != n} Gamma^(n,m)[b, a] z_m[b + R a]); flm-b: f = z.
 template <class T>
 __global__ void k_apply_k(const T* __restrict__ z, int N, int R, const T* __restrict__ pair, T* __restrict__ f,
