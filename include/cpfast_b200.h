@@ -105,6 +105,16 @@ int cpf_nccl_unique_id(void* out128);
 int cpf_engine_create(cpf_engine** out, int device, int kind, int order, const int64_t* dims, int rank,
                       int world_rank, int world_size, const void* nccl_uid128);
 void cpf_engine_destroy(cpf_engine* e);
+/* TEST TRANSPORT (no reference counterpart): a loopback group of `world` engines in ONE process on
+ * one device, each driven by its own host thread, whose collectives (the same allreduce /
+ * allgather / broadcast the NCCL path issues) exchange through device buffers ordered by CUDA
+ * events and a host barrier -- no kernel waits on another rank's kernel.  It runs the multi-rank
+ * data path (slab bounds, ragged slabs, packed allreduce, allgather reorder, sharded mode-N Gram)
+ * without a multi-GPU box.  Loopback engines launch eagerly (no CUDA graph). */
+int cpf_loopback_group_create(int world, void** group);
+void cpf_loopback_group_destroy(void* group);
+int cpf_engine_create_loopback(cpf_engine** out, int device, int kind, int order, const int64_t* dims, int rank,
+                               int world_rank, void* group);
 const char* cpf_engine_last_error(const cpf_engine* e);
 /* Local slab [lo, hi) of mode N owned by this rank. */
 int cpf_engine_slab(const cpf_engine* e, int64_t* lo, int64_t* hi);
@@ -170,7 +180,8 @@ int cpf_pinv_psd(int device, int kind, int R, const void* gram, void* out);
 int cpf_engine_profile(cpf_engine* e, int enable);
 int cpf_engine_phase_times(cpf_engine* e, double* ms_out, int64_t* counts_out, int nphases);
 /* G_n = Y_(n) Y_(n)^H (I_n x I_n, column-major) of the bound tensor, for the SVD initialisation
- * (kruskal.py:227-242).  Sharded tensors: modes 1..N-1 only. */
+ * (kruskal.py:227-242).  Sharded tensors: every mode (mode N by broadcasting each slab in turn;
+ * every rank returns the full matrix). */
 int cpf_engine_unfolding_gram(cpf_engine* e, int mode, void* out);
 /* Number of kernels this engine has launched (for the bench's gpu_launches count). */
 int64_t cpf_engine_launch_count(const cpf_engine* e);

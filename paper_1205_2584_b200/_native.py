@@ -70,6 +70,9 @@ EXPORTED_SYMBOLS = (
     "cpf_engine_als_step",
     "cpf_engine_set_history",
     "cpf_engine_fast_damped_inverse",
+    "cpf_loopback_group_create",
+    "cpf_loopback_group_destroy",
+    "cpf_engine_create_loopback",
     "cpf_pinv_psd",
     "cpf_device_count",
     "cpf_nccl_unique_id",
@@ -149,6 +152,9 @@ def _declare(lib) -> None:
         "cpf_engine_set_history": (I, [P, P]),
         "cpf_pinv_psd": (I, [I, I, I, P, P]),
         "cpf_engine_fast_damped_inverse": (I, [P, D, I, P, P, ctypes.POINTER(I)]),
+        "cpf_loopback_group_create": (I, [I, ctypes.POINTER(P)]),
+        "cpf_loopback_group_destroy": (None, [P]),
+        "cpf_engine_create_loopback": (I, [ctypes.POINTER(P), I, I, I, ctypes.POINTER(I64), I, I, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -167,7 +173,14 @@ def load():
                 f"{LIB_PATH} is missing: build the CUDA engine first "
                 "(python -c 'import __graft_entry__ as g; g.build()').  There is no CPU fallback."
             )
-        # NCCL is resolved by soname; if torch is loaded first its bundled libnccl serves it.
+        # NCCL is resolved by soname.  torch (the device-memory / torch.distributed plumbing) bundles
+        # a newer libnccl than the system one; load it first so that one library serves both --
+        # the other order leaves the older system NCCL global and a later `import torch` fails
+        # (undefined symbol ncclDevCommCreate).
+        try:
+            import torch  # noqa: F401
+        except ImportError:  # pragma: no cover - the engine itself does not need torch
+            pass
         lib = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_GLOBAL if hasattr(os, "RTLD_GLOBAL") else 0)
         _declare(lib)
         _lib = lib
@@ -230,11 +243,37 @@ def _raise_for(rc: int, msg: str):
     raise NativeError(f"native engine error {rc}: {msg}")
 
 
+class LoopbackGroup:
+    """Test transport: ``world`` engines of this process on one device exchanging through device
+    buffers (cpf_loopback_group_create).  Drive each rank's engine from its own thread."""
+
+    def __init__(self, world: int):
+        lib = load()
+        self._lib = lib
+        self.world = int(world)
+        h = ctypes.c_void_p()
+        rc = lib.cpf_loopback_group_create(self.world, ctypes.byref(h))
+        if rc != CPF_OK:
+            _raise_for(rc, f"loopback group of {world} ranks")
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self._lib.cpf_loopback_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Engine:
     """One native fit context on one GPU (owns device buffers; not thread-safe)."""
 
     def __init__(self, kind: int, dims, rank: int, device: int = 0, world_rank: int = 0, world_size: int = 1,
-                 nccl_uid: bytes | None = None):
+                 nccl_uid: bytes | None = None, loopback: LoopbackGroup | None = None):
         lib = load()
         self._lib = lib
         self.kind = kind
@@ -243,9 +282,13 @@ class Engine:
         self.dtype = np.complex128 if kind == CPF_COMPLEX else np.float64
         arr = (ctypes.c_int64 * len(self.dims))(*self.dims)
         h = ctypes.c_void_p()
-        uid = ctypes.create_string_buffer(nccl_uid, 128) if nccl_uid is not None else None
-        rc = lib.cpf_engine_create(ctypes.byref(h), int(device), int(kind), len(self.dims), arr, self.rank,
-                                   int(world_rank), int(world_size), uid)
+        if loopback is not None:
+            rc = lib.cpf_engine_create_loopback(ctypes.byref(h), int(device), int(kind), len(self.dims), arr,
+                                                self.rank, int(world_rank), loopback.handle)
+        else:
+            uid = ctypes.create_string_buffer(nccl_uid, 128) if nccl_uid is not None else None
+            rc = lib.cpf_engine_create(ctypes.byref(h), int(device), int(kind), len(self.dims), arr, self.rank,
+                                       int(world_rank), int(world_size), uid)
         if rc != CPF_OK:
             msg = lib.cpf_engine_last_error(h).decode() if h.value else "engine creation failed"
             if h.value:
@@ -377,7 +420,7 @@ class Engine:
         return list(ms), list(cnt)
 
     def unfolding_gram(self, mode: int) -> np.ndarray:
-        d = self.dims[mode - 1] if mode < len(self.dims) else (self.slab[1] - self.slab[0])
+        d = self.dims[mode - 1]  # sharded mode N: every rank receives the full I_N x I_N Gram
         out = np.empty((d, d), dtype=self.dtype, order="F")
         self._check(self._lib.cpf_engine_unfolding_gram(self._h, int(mode), out.ctypes.data))
         return out

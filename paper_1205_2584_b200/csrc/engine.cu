@@ -51,6 +51,8 @@ struct ApiError : std::runtime_error {
     if (_r != ncclSuccess) throw ApiError(CPF_E_NCCL, std::string("NCCL error ") + ncclGetErrorString(_r) + " (" #expr ")"); \
   } while (0)
 
+#include "comm.cuh"
+
 namespace cpf {
 
 static int padded_rank(int R) {
@@ -105,7 +107,7 @@ struct Engine final : EngineBase {
   cudaStream_t s3 = nullptr;   // pass B + gradient of an accepted step, overlapped with the next LU
   cudaEvent_t evF = nullptr, evG = nullptr;
   const bool serial = [] { const char* e = getenv("CPF_SERIAL"); return e && e[0] == '1'; }();
-  ncclComm_t comm = nullptr;
+  std::unique_ptr<Comm> comm;  // NCCL (world > 1) or the loopback test transport; null: 1 rank
   int64_t nlaunch = 0;
 
   // ---- tensor
@@ -219,7 +221,8 @@ struct Engine final : EngineBase {
   int64_t ph_cnt[kNumPhases] = {0};
 
   // ------------------------------------------------------------------------------------------
-  Engine(int device, int order, const int64_t* d, int rank, int wr, int ws, const void* uid) {
+  Engine(int device, int order, const int64_t* d, int rank, int wr, int ws, const void* uid,
+         LoopbackGroup* loop = nullptr) {
     if (order < 2 || order > kMaxModes) throw ApiError(CPF_E_UNSUPPORTED, "order must be in [2, 8]");
     if (rank < 1) throw ApiError(CPF_E_ARG, "rank must be >= 1");
     RP = padded_rank(rank);
@@ -267,7 +270,13 @@ struct Engine final : EngineBase {
     // communicator, packed allreduce / allgather / reorder kernels) so it can be tested on 1 GPU.
     const char* fe = getenv("CPF_FORCE_NCCL");
     const bool force = fe && fe[0] == '1';
-    if (world > 1 || force) {
+    if (loop) {
+      // loopback test transport: P engines of one process on one GPU (comm.cuh); its host
+      // barriers cannot live inside a captured graph, so these engines launch eagerly
+      if (loop->world != world || wrank < 0 || wrank >= world) throw ApiError(CPF_E_ARG, "loopback group / rank mismatch");
+      comm.reset(new LoopbackComm(loop, wrank));
+      graph_ok = false;
+    } else if (world > 1 || force) {
       ncclUniqueId id;
       if (world > 1) {
         if (!uid) throw ApiError(CPF_E_ARG, "world_size > 1 needs an NCCL unique id");
@@ -275,7 +284,7 @@ struct Engine final : EngineBase {
       } else {
         NCCL_CHECK(ncclGetUniqueId(&id));
       }
-      NCCL_CHECK(ncclCommInitRank(&comm, world, id, wrank));
+      comm.reset(new NcclComm(world, id, wrank));
     }
     configure_pool(dev);
     alloc();
@@ -308,7 +317,7 @@ struct Engine final : EngineBase {
     for (void* p : ptrs)
       if (p) cudaFreeAsync(p, s);  // back to the device pool (kept for the next engine)
     if (hst) cudaFreeHost(hst);
-    if (comm) ncclCommDestroy(comm);
+    comm.reset();
     if (s) cudaStreamDestroy(s);
   }
 
@@ -946,10 +955,7 @@ struct Engine final : EngineBase {
       }
     }
     if (!oz) pass_a_fp64(F, gate);
-    if (comm) {
-      NCCL_CHECK(ncclAllReduce(pa_out, pa_out, (size_t)(I1 + Lmid) * R * (sizeof(T) / sizeof(double)), ncclDouble,
-                               ncclSum, comm, s));
-    }
+    if (comm) comm->allreduce_sum((double*)pa_out, (size_t)(I1 + Lmid) * R * (sizeof(T) / sizeof(double)), s);
     // scatter: M_1 = pa_out[0 : I1 R]; N==3: M_2 = Z; N>=4: M_2..M_{N-1} from Z (at F)
     launch(k_copy<T>, nblocks(I1 * R, 256), 256, 0, (const T*)pa_out, Mout + offs[0], I1 * R, (const LmDeviceState*)st, (const DevFlags*)fl, gate);
     if (N == 3) {
@@ -1058,7 +1064,7 @@ struct Engine final : EngineBase {
       CPF_CUDA_CHECK(cudaMemsetAsync(pb_out, 0, sizeof(T) * Cpad * R, ls));
       if (Cloc > 0) mn_rows(pb_out, Cpad);
       const size_t cnt = (size_t)Cpad * R * (sizeof(T) / sizeof(double));
-      NCCL_CHECK(ncclAllGather(pb_out, pb_all, cnt, ncclDouble, comm, ls));
+      comm->allgather((const double*)pb_out, (double*)pb_all, cnt, ls);
       // pb_all[rank][c + Cpad r] -> Mout_N[(rank*Cpad + c) + IN r]
       for (int q = 0; q < world; ++q) {
         const int64_t lo = std::min<int64_t>(IN, (int64_t)q * Cpad);
@@ -1146,7 +1152,7 @@ struct Engine final : EngineBase {
       launch(k_axpby<double>, 1, 1, 0, (const double*)out, 0.0, (const double*)nullptr, 0.0, out, (int64_t)1, cst, cfl,
              gate);
     }
-    if (comm) NCCL_CHECK(ncclAllReduce(out, out, 1, ncclDouble, ncclSum, comm, s));
+    if (comm) comm->allreduce_sum(out, 1, s);
   }
 
   // ------------------------------------------------------------------------------------------
@@ -1453,7 +1459,7 @@ struct Engine final : EngineBase {
     } else {
       CPF_CUDA_CHECK(cudaMemsetAsync(dscal + 1, 0, sizeof(double), s));
     }
-    if (comm) NCCL_CHECK(ncclAllReduce(dscal + 1, dscal + 1, 1, ncclDouble, ncclSum, comm, s));
+    if (comm) comm->allreduce_sum(dscal + 1, 1, s);
     double v;
     CPF_CUDA_CHECK(cudaMemcpyAsync(&v, dscal + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
     CPF_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -1637,7 +1643,9 @@ struct Engine final : EngineBase {
     // cancellation error at no measurable cost (config 1 regime).
     {
       const double cw = sizeof(T) == 16 ? 4.0 : 1.0;
-      const double pass_flops = 2.0 * cw * (double)Jloc * world * R;
+      // global J, not Jloc * world: identical on every rank of a ragged split (the choice decides
+      // which collectives the iteration issues)
+      const double pass_flops = 2.0 * cw * (double)Lrows * IN * R;
       const double lu_flops = (2.0 / 3.0) * cw * (double)nB * nB * nB;
       hst->force_direct = pass_flops < 0.05 * lu_flops ? 1 : 0;
       if (const char* e = getenv("CPF_FORCE_DIRECT")) hst->force_direct = (e[0] == '1');
@@ -1896,33 +1904,69 @@ struct Engine final : EngineBase {
     if (rejected) *rejected = oz_y_rejected ? 1 : 0;
   }
 
-  // G_n = Y_(n) Y_(n)^H on the device (sum of the slab partials across ranks for n < N)
+  // Partial Gram block  Ya_(n) Yb_(n)^H  (Ina x Inb) -> out (device, column-major, ld Ina)
+  void gram_block(const T* Ya, const T* Yb, int64_t P, int64_t Ina, int64_t Inb, int64_t Q, T* out) {
+    const int64_t K = P * Q;
+    const int ta = (int)((Ina + 31) / 32), tb = (int)((Inb + 31) / 32);
+    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>((K + 4095) / 4096, (148 * 8) / std::max(1, ta * tb) + 1));
+    const int64_t kchunk = ((K + nsplit - 1) / nsplit + 31) / 32 * 32;
+    nsplit = (int)((K + kchunk - 1) / kchunk);
+    T* part = nullptr;
+    CPF_CUDA_CHECK(cudaMallocAsync(&part, sizeof(T) * (size_t)nsplit * Ina * Inb, s));
+    launch(k_unfold_gram<T>, dim3(ta * tb, nsplit), 256, 0, Ya, Yb, P, Ina, Inb, Q, kchunk, part);
+    launch(k_gram_reduce<T>, nblocks(Ina * Inb, 256), 256, 0, (const T*)part, nsplit, Ina * Inb, out);
+    CPF_CUDA_CHECK(cudaFreeAsync(part, s));
+  }
+
+  // G_n = Y_(n) Y_(n)^H on the device.  Modes n < N: every rank's slab gives a partial sum over
+  // its columns, allreduced.  Mode N of a sharded tensor: the rows of Y_(N) are split across
+  // ranks, so rank p forms its block row G[slab_p, :] against every rank's slab (each slab
+  // broadcast in turn from its owner) and the block rows are summed across ranks.
   void unfolding_gram(int mode, void* out) override {
     if (!have_tensor) throw ApiError(CPF_E_STATE, "no tensor bound");
     if (mode < 1 || mode > N) throw ApiError(CPF_E_ARG, "mode out of range");
-    if (mode == N && world > 1) throw ApiError(CPF_E_UNSUPPORTED, "mode-N Gram of a sharded tensor");
     const int n = mode - 1;
+    const size_t words = sizeof(T) / sizeof(double);
+    if (mode == N && comm && world > 1) {
+      T* G = nullptr;
+      T* Yq = nullptr;
+      T* blk = nullptr;
+      CPF_CUDA_CHECK(cudaMallocAsync(&G, sizeof(T) * (size_t)IN * IN, s));
+      CPF_CUDA_CHECK(cudaMemsetAsync(G, 0, sizeof(T) * (size_t)IN * IN, s));
+      CPF_CUDA_CHECK(cudaMallocAsync(&Yq, sizeof(T) * (size_t)std::max<int64_t>(1, Lrows * Cpad), s));
+      CPF_CUDA_CHECK(cudaMallocAsync(&blk, sizeof(T) * (size_t)std::max<int64_t>(1, Cpad * Cpad), s));
+      for (int q = 0; q < world; ++q) {
+        const int64_t lo = std::min<int64_t>(IN, (int64_t)q * Cpad);
+        const int64_t cnt = std::min<int64_t>(IN, lo + Cpad) - lo;
+        if (cnt <= 0) continue;
+        comm->broadcast(q == wrank ? (const double*)Y : nullptr, (double*)Yq, (size_t)(Lrows * cnt) * words, q, s);
+        if (Cloc <= 0) continue;
+        gram_block(Y, Yq, Lrows, Cloc, cnt, 1, blk);
+        launch(k_copy2d<T>, nblocks(Cloc * cnt, 256), 256, 0, (const T*)blk, Cloc, G + slab_lo + IN * lo, IN, Cloc, cnt,
+               (const LmDeviceState*)st, (const DevFlags*)fl, (int)kAlways);
+      }
+      comm->allreduce_sum((double*)G, (size_t)IN * IN * words, s);
+      CPF_CUDA_CHECK(cudaMemcpyAsync(out, G, sizeof(T) * IN * IN, cudaMemcpyDeviceToHost, s));
+      CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+      cudaFreeAsync(G, s);
+      cudaFreeAsync(Yq, s);
+      cudaFreeAsync(blk, s);
+      CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+      return;
+    }
     int64_t P = 1, Q = 1;
     for (int k = 0; k < n; ++k) P *= dims[k];
     for (int k = n + 1; k < N; ++k) Q *= (k == N - 1) ? Cloc : dims[k];
     const int64_t In = (n == N - 1) ? Cloc : dims[n];
-    const int64_t K = P * Q;
-    const int ntile = (int)((In + 31) / 32);
-    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>((K + 4095) / 4096, (148 * 8) / std::max(1, ntile * ntile) + 1));
-    const int64_t kchunk = ((K + nsplit - 1) / nsplit + 31) / 32 * 32;
-    nsplit = (int)((K + kchunk - 1) / kchunk);
-    T* part = nullptr;
     T* G = nullptr;
-    CPF_CUDA_CHECK(cudaMalloc(&part, sizeof(T) * (size_t)nsplit * In * In));
-    CPF_CUDA_CHECK(cudaMalloc(&G, sizeof(T) * (size_t)In * In));
-    launch(k_unfold_gram<T>, dim3(ntile * ntile, nsplit), 256, 0, Y, P, In, Q, kchunk, part);
-    launch(k_gram_reduce<T>, nblocks(In * In, 256), 256, 0, (const T*)part, nsplit, In * In, G);
-    if (comm && mode < N)
-      NCCL_CHECK(ncclAllReduce(G, G, (size_t)In * In * (sizeof(T) / sizeof(double)), ncclDouble, ncclSum, comm, s));
+    CPF_CUDA_CHECK(cudaMallocAsync(&G, sizeof(T) * (size_t)In * In, s));
+    if (Jloc > 0) gram_block(Y, Y, P, In, In, Q, G);
+    else CPF_CUDA_CHECK(cudaMemsetAsync(G, 0, sizeof(T) * (size_t)In * In, s));
+    if (comm && mode < N) comm->allreduce_sum((double*)G, (size_t)In * In * words, s);
     CPF_CUDA_CHECK(cudaMemcpyAsync(out, G, sizeof(T) * In * In, cudaMemcpyDeviceToHost, s));
     CPF_CUDA_CHECK(cudaStreamSynchronize(s));
-    cudaFree(part);
-    cudaFree(G);
+    cudaFreeAsync(G, s);
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
   }
 
   // ------------------------------------------------------------------------------------------
@@ -2134,6 +2178,42 @@ int cpf_engine_create(cpf_engine** out, int device, int kind, int order, const i
   }
   *out = e;
   return CPF_OK;
+}
+
+int cpf_loopback_group_create(int world, void** out) {
+  if (!out) return CPF_E_ARG;
+  *out = nullptr;
+  try {
+    *out = new cpf::LoopbackGroup(world);
+    return CPF_OK;
+  } catch (const ApiError& x) {
+    g_create_error = x.what();
+    return x.code;
+  } catch (const std::exception& x) {
+    g_create_error = x.what();
+    return CPF_E_CUDA;
+  }
+}
+
+void cpf_loopback_group_destroy(void* group) { delete static_cast<cpf::LoopbackGroup*>(group); }
+
+int cpf_engine_create_loopback(cpf_engine** out, int device, int kind, int order, const int64_t* dims, int rank,
+                               int world_rank, void* group) {
+  if (!out || !group) return CPF_E_ARG;
+  *out = nullptr;
+  auto* g = static_cast<cpf::LoopbackGroup*>(group);
+  auto* e = new cpf_engine();
+  int rc = guarded(nullptr, [&] {
+    if (kind == CPF_REAL)
+      e->impl.reset(new cpf::Engine<double>(device, order, dims, rank, world_rank, g->world, nullptr, g));
+    else if (kind == CPF_COMPLEX)
+      e->impl.reset(new cpf::Engine<cplx>(device, order, dims, rank, world_rank, g->world, nullptr, g));
+    else
+      throw ApiError(CPF_E_KIND, "unknown scalar kind");
+  });
+  if (rc != CPF_OK) e->err = g_create_error;
+  *out = e;
+  return rc;
 }
 
 void cpf_engine_destroy(cpf_engine* e) { delete e; }

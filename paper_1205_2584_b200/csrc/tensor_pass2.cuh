@@ -378,11 +378,14 @@ namespace cpf {
 // Unfolding Gram G_n = Y_(n) Y_(n)^H (I_n x I_n) for the SVD initialisation (kruskal.py:227-242:
 // the leading left singular vectors of Y_(n) are the leading eigenvectors of G_n).
 // Y_(n)[i, k] with k = a + P b  ->  Y[a + P i + P I_n b]  (a over modes < n, b over modes > n).
-// grid (tiles_i * tiles_i, ksplit); 32x32 output tile per CTA, 256 threads x (2x2); per-CTA partial
-// tiles are summed by k_gram_reduce in fixed order.
+// grid (tiles_i * tiles_j, ksplit); 32x32 output tile per CTA, 256 threads x (2x2); per-CTA partial
+// tiles are summed by k_gram_reduce in fixed order.  Cross form (sharded mode-N Gram): the
+// column operand comes from Yb with Inb columns, G = Y_(n) Yb_(n)^H (In x Inb); Yb = Y, Inb = In
+// is the plain Gram.
 template <class T>
-__global__ void __launch_bounds__(256) k_unfold_gram(const T* __restrict__ Y, int64_t P, int64_t In, int64_t Q,
-                                                     int64_t kchunk, T* __restrict__ part) {
+__global__ void __launch_bounds__(256) k_unfold_gram(const T* __restrict__ Y, const T* __restrict__ Yb, int64_t P,
+                                                     int64_t In, int64_t Inb, int64_t Q, int64_t kchunk,
+                                                     T* __restrict__ part) {
   pdl_wait();
   __shared__ T As[32][33];
   __shared__ T Bs[32][33];
@@ -407,7 +410,7 @@ __global__ void __launch_bounds__(256) k_unfold_gram(const T* __restrict__ Y, in
         const int64_t a = k % P, b = k / P;
         const int64_t base = a + P * In * b;
         if (gi < In) va = Y[base + P * gi];
-        if (gj < In) vb = Y[base + P * gj];
+        if (gj < Inb) vb = Yb[base + P * gj];
       }
       As[kk][ii] = va;
       Bs[kk][ii] = vb;
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(256) k_unfold_gram(const T* __restrict__ Y, in
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       const int64_t gi = (int64_t)ti * 32 + ty + 16 * u, gj = (int64_t)tj * 32 + tx + 16 * v;
-      if (gi < In && gj < In) part[((int64_t)blockIdx.y * In + gj) * In + gi] = acc[u][v];  // column-major
+      if (gi < In && gj < Inb) part[((int64_t)blockIdx.y * Inb + gj) * In + gi] = acc[u][v];  // column-major
     }
 }
 

@@ -187,6 +187,25 @@ class _Dist:
         return obj[0]
 
 
+class LoopbackRank:
+    """``distributed=`` handle of the loopback TEST transport: rank ``rank`` of a
+    ``_native.LoopbackGroup`` -- several ranks' engines in one process on one GPU, each fit driven
+    from its own thread, exchanging through device buffers (include/cpfast_b200.h)."""
+
+    def __init__(self, group, rank: int):
+        self.group, self.rank, self.world = group, int(rank), group.world
+
+
+def _engine_for(kind: int, dims, rank: int, dev: int, distributed):
+    if distributed is None:
+        return _native.Engine(kind, dims, rank, dev)
+    if isinstance(distributed, LoopbackRank):
+        return _native.Engine(kind, dims, rank, dev, distributed.rank, distributed.world, loopback=distributed.group)
+    ctx = distributed if isinstance(distributed, _Dist) else _Dist(distributed if distributed is not True else None)
+    uid = ctx.unique_id() if ctx.world > 1 else None
+    return _native.Engine(kind, dims, rank, dev, ctx.rank, ctx.world, uid)
+
+
 def slab_bounds(dim_n: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous slab of the last mode owned by ``rank`` (ceil split, same rule as the engine)."""
     per = -(-dim_n // world)
@@ -199,12 +218,7 @@ def _make_engine(y: DenseTensor, rank: int, device, distributed, slab_of=None):
     if len(dims) < 2:
         raise ValueError("the fLM solver needs a tensor of order >= 2")
     dev = 0 if device is None else int(device)
-    if distributed is not None:
-        ctx = distributed if isinstance(distributed, _Dist) else _Dist(distributed if distributed is not True else None)
-        uid = ctx.unique_id() if ctx.world > 1 else None
-        eng = _native.Engine(_kind_code(y.data), dims, rank, dev, ctx.rank, ctx.world, uid)
-    else:
-        eng = _native.Engine(_kind_code(y.data), dims, rank, dev)
+    eng = _engine_for(_kind_code(y.data), dims, rank, dev, distributed)
     lo, hi = eng.slab
     if slab_of is None:
         eng.set_tensor_host(y.data[..., lo:hi])
@@ -341,12 +355,7 @@ def fit_file(path, config: FitConfig, *, device=None, distributed=None, complex_
         raise TypeError("expected a complex tensor")
     kind = _native.CPF_COMPLEX if h.kind else _native.CPF_REAL
     dev = 0 if device is None else int(device)
-    if distributed is not None:
-        ctx = distributed if isinstance(distributed, _Dist) else _Dist(distributed if distributed is not True else None)
-        uid = ctx.unique_id() if ctx.world > 1 else None
-        eng = _native.Engine(kind, h.dims, config.rank, dev, ctx.rank, ctx.world, uid)
-    else:
-        eng = _native.Engine(kind, h.dims, config.rank, dev)
+    eng = _engine_for(kind, h.dims, config.rank, dev, distributed)
     try:
         cptn.load_to_engine(eng, path, h)
     except BaseException:
