@@ -88,6 +88,7 @@ __device__ __forceinline__ cplx ld_ro(const cplx* p) {
   return cplx{v.x, v.y};
 }
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ int ld_cg(const int* p) { return __ldcg(p); }
 __device__ __forceinline__ cplx ld_cg(const cplx* p) {
   double2 v = __ldcg(reinterpret_cast<const double2*>(p));
   return cplx{v.x, v.y};

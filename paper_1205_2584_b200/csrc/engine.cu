@@ -35,6 +35,7 @@ struct ApiError : std::runtime_error {
 #include "lu.cuh"
 #include "lu3.cuh"
 #include "lu4.cuh"
+#include "lu_persist.cuh"
 #include "tri_inv.cuh"
 #include "phi.cuh"
 #include "small_ops.cuh"
@@ -313,7 +314,8 @@ struct Engine final : EngineBase {
                     wvec, fvec, xvec, Phi, A1c, KMc, WNc, A1r, KMr, WNr, zpart, m1part, bpart, pa_out, pb_out, pb_all,
                     norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL, WNd, KMd, gring, PhiInv, TriTmp, yvec, tmv_part,
                     ozYA, ozYB, ozBA, ozBB, ozFrowA, ozFrowB, ozFr, ozM1, ozZ, ozBp,
-                    PhiS, PhiInvS, TriTmpS, GtiS, GiS, invLS, ibufS, gringS, spec_sing, Hist, Pinv};
+                    PhiS, PhiInvS, TriTmpS, GtiS, GiS, invLS, ibufS, gringS, spec_sing, Hist, Pinv,
+                    lp.panel_done, lp.u12s, lpS.panel_done, lpS.u12s};
     for (void* p : ptrs)
       if (p) cudaFreeAsync(p, s);  // back to the device pool (kept for the next engine)
     if (hst) cudaFreeHost(hst);
@@ -452,6 +454,7 @@ struct Engine final : EngineBase {
     }
     lu_smem = panel_smem_bytes<T>(lu_rpc, lu_kb, lu_cl);
     plan_lu3();
+    plan_lp();
     plan_v2(nsm);
     plan_dmma(nsm);
     plan_oz();
@@ -467,6 +470,67 @@ struct Engine final : EngineBase {
 
   int lu3_thr = 128;  // threads per CTA of the register panel
   // rotating-frame panel (lu4.cuh): rows/thread and threads/CTA; 0 = use k_panel_lu3
+  // LU v5 (lu_persist.cuh): the whole factorization in one persistent kernel, panel rows in one
+  // CTA's registers (n_B <= 1280 real / 512 complex).  EXPERIMENTAL, off by default (CPF_LU=5):
+  // measured slower than the v4 path (n_B = 1200 alone: 2.05-2.14 vs 1.46 ms for LU + inverses,
+  // profiles/r02_lu_persist.txt) -- the single-CTA column loop costs ~2700 cycles per column,
+  // no better than v4's cluster exchange, and its 16-column steps double the step count.
+  // lp_cfg: 0 off, else the (threads, rows per thread) instantiation.
+  int lp_cfg = 0, lp_grid = 0;
+  LuPersist lp{}, lpS{};
+  void alloc_lp(LuPersist& q) {
+    const int np = (nB + kLpKB - 1) / kLpKB;
+    q.n = nB;
+    q.np = np;
+    int* ib = dalloc<int>((size_t)3 * np + nB + (size_t)np * kLpKB + 4);
+    q.panel_done = ib;
+    q.block_ready = ib + np;
+    q.blk_done = ib + 2 * np;
+    q.ret = ib + 3 * np;
+    q.piv = q.ret + nB;
+    q.bar = q.piv + (size_t)np * kLpKB;
+    q.u12s = dalloc<T>((size_t)np * kLpKB * kLpKB);
+  }
+  void plan_lp() {
+    const char* e = getenv("CPF_LU");
+    if (!(e && e[0] == '5')) return;
+    if (!use_inv) return;  // the final gather uses TriTmp (allocated with the explicit inverse)
+    if constexpr (sizeof(T) == 8) {
+      lp_cfg = nB <= 512 ? 1 : nB <= 1024 ? 2 : nB <= 1280 ? 3 : 0;
+    } else {
+      lp_cfg = nB <= 512 ? 11 : 0;
+    }
+    if (!lp_cfg) return;
+    lp_dispatch([&](auto kern, int) {
+      CPF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lp_smem_bytes<T>(nB)));
+    });
+    alloc_lp(lp);
+    lp.perm = lu.perm;
+    lp.info = lu.info;
+    lp.tmp = TriTmp;
+  }
+  template <class F>
+  void lp_dispatch(F&& f) {
+    if constexpr (sizeof(T) == 8) {
+      if (lp_cfg == 1) f(k_lu_persist<T, 256, 2>, 256);
+      else if (lp_cfg == 2) f(k_lu_persist<T, 256, 4>, 256);
+      else f(k_lu_persist<T, 256, 5>, 256);
+    } else {
+      f(k_lu_persist<T, 256, 2>, 256);
+    }
+  }
+  void lu_factor_lp(int gate_running) {
+    const LuPersist& q = lp;
+    const int np = q.np;
+    // helpers: the SMs the fork leaves to the LU, at most one per column block
+    LuPersist a = q;
+    a.nhelp = std::max(1, std::min(std::max(1, kLuReserveSms - 1), np));
+    launch(k_lp_init, nblocks(std::max(nB, np), 256), 256, 0, a);
+    lp_dispatch([&](auto kern, int nt) {
+      launch(kern, dim3(1 + a.nhelp), dim3(nt), lp_smem_bytes<T>(nB), Phi, a, (const LmDeviceState*)st, gate_running);
+    });
+  }
+
   static constexpr int kLu4Rpt = sizeof(T) == 8 ? 2 : 1;
   static constexpr int kLu4Thr = 256;
   bool use_lu4 = false;
@@ -649,6 +713,12 @@ struct Engine final : EngineBase {
     luS.ticket = luS.info + 1;
     luS.ready = luS.ticket + 4;
     spec_sing = dalloc<int>(2);
+    if (lp_cfg) {
+      alloc_lp(lpS);
+      lpS.perm = luS.perm;
+      lpS.info = luS.info;
+      lpS.tmp = TriTmpS;
+    }
     int plo = 0, phi = 0;
     CPF_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&plo, &phi));
     CPF_CUDA_CHECK(cudaStreamCreateWithPriority(&sS, cudaStreamNonBlocking, phi));
@@ -665,6 +735,7 @@ struct Engine final : EngineBase {
     std::swap(invL, invLS);
     std::swap(gring, gringS);
     std::swap(lu, luS);
+    std::swap(lp, lpS);
     std::swap(s, sS);
     std::swap(s2, sS2);
   }
@@ -1223,6 +1294,12 @@ struct Engine final : EngineBase {
 
   void lu_factor(int gate_running) {
     ph_begin(kPhLU);
+    if (lp_cfg) {
+      lu_factor_lp(gate_running);
+      if (!spec_capture) launch(k_lu_info_to_err, 1, 1, 0, (const int*)lu.info, st);
+      ph_end();
+      return;
+    }
     launch(k_lu_init, nblocks(nB, 256), 256, 0, lu.perm, nB, lu.info);
     if (lu3_rpt) {
       // Look-ahead right-looking LU.  Panel k+1's columns are the "next block" of step k: the
@@ -2368,6 +2445,6 @@ extern "C" int cpf_debug_lu_trace(int on, unsigned long long* out) {
 }
 
 extern "C" int cpf_debug_panel_cycles(long long* out12) {
-  if (cudaMemcpyFromSymbol(out12 + 8, cpf::g_panel_seg, sizeof(long long) * 8) != cudaSuccess) return -4;
+  if (cudaMemcpyFromSymbol(out12 + 8, cpf::g_panel_seg, sizeof(long long) * 12) != cudaSuccess) return -4;
   return cudaMemcpyFromSymbol(out12, cpf::g_panel_cycles, sizeof(long long) * 8) == cudaSuccess ? 0 : -4;
 }

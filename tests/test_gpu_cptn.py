@@ -87,10 +87,23 @@ def test_cli_fit_writes_factors_and_record(api, tmp_path):
 
 
 def test_cli_rejects_cpu_only_variants(api, tmp_path):
+    """dgn-oracle (the dense desk-scale oracle) stays CPU-only; ALS runs on the engine."""
     from paper_1205_2584_b200 import cptn
     from paper_1205_2584_b200.cli import main
 
     cptn.write_tensor(tmp_path / "t.cptn", api.DenseTensor(np.ones((3, 3, 3))))
-    res = CliRunner().invoke(main, ["fit", str(tmp_path / "t.cptn"), "--rank", "2", "--algo", "als"])
+    res = CliRunner().invoke(main, ["fit", str(tmp_path / "t.cptn"), "--rank", "2", "--algo", "dgn-oracle"])
     assert res.exit_code == 1
     assert "not supported on the B200 backend" in res.output
+
+
+def test_cli_fit_als(api, tmp_path):
+    from paper_1205_2584_b200 import cptn
+    from paper_1205_2584_b200.cli import main
+
+    rng = np.random.default_rng(3)
+    y = np.einsum("ir,jr,kr->ijk", *(rng.standard_normal((d, 2)) for d in (4, 5, 6)))
+    cptn.write_tensor(tmp_path / "t.cptn", api.DenseTensor(np.asfortranarray(y)))
+    res = CliRunner().invoke(main, ["fit", str(tmp_path / "t.cptn"), "--rank", "2", "--algo", "als-ls",
+                                    "--max-iters", "30", "--init", "random"])
+    assert res.exit_code == 0, res.output

@@ -71,6 +71,6 @@ def test_cli_bench_writes_records_and_summary(engine_lib, tmp_path):
     assert res.exit_code == 0, res.output
     rows = _rows(out)
     assert list(rows[0].keys()) == list(CSV_COLUMNS) and len(rows) == 4
-    assert [r["stop_reason"] for r in rows if r["algo"] == "als-ls"] == ["error", "error"]  # CPU-only variant
+    assert all(r["stop_reason"] in ("tol", "max_iters") for r in rows if r["algo"] == "als-ls")
     assert all(r["stop_reason"] in ("tol", "max_iters") for r in rows if r["algo"] == "auto")
     assert (tmp_path / "b_summary.csv").exists() and "median_iters=" in res.output

@@ -72,7 +72,7 @@ def _trace(res):
     return [(r.iter, r.relerr, r.mu, r.accepted) for r in res.trace]
 
 
-def _compare(single, ranks, tag, fac_tol=1e-10):
+def _compare(single, ranks, tag, fac_tol=1e-10, err_tol=1e-12):
     for r, res in enumerate(ranks):
         assert _trace(res) == _trace(ranks[0]), f"{tag}: rank {r} differs from rank 0"
         assert np.array_equal(res.model.as_vector(), ranks[0].model.as_vector())
@@ -83,7 +83,7 @@ def _compare(single, ranks, tag, fac_tol=1e-10):
     v, w = res.model.as_vector(), single.model.as_vector()
     d_fac = float(np.linalg.norm(v - w) / np.linalg.norm(w))
     print(f"{tag}: max |relerr diff| {d_err:.2e}, factor rel diff {d_fac:.2e}")
-    assert d_err < 1e-12, tag
+    assert d_err < err_tol, tag
     assert d_fac < fac_tol, tag
 
 
@@ -111,7 +111,8 @@ def test_sharded_svd_init(api, case):
     across ranks (slab broadcasts), so the default FitConfig works distributed."""
     cfg, y, tau, _ = _problem(case)
     conf = api.FitConfig(rank=cfg.rank, tau=tau, tol=0.0, max_iters=12, seed=0, init="svd")
-    _compare(api.fit(y, conf), _sharded_fit(api, y, conf, 3), f"{case} svd P=3", fac_tol=1e-9)
+    # the unfolding Grams' slab sums change order; the eigenvectors move by ~1e-12 (init only)
+    _compare(api.fit(y, conf), _sharded_fit(api, y, conf, 3), f"{case} svd P=3", fac_tol=1e-9, err_tol=1e-10)
 
 
 @pytest.mark.parametrize("variant", ["als", "als-ls"])
