@@ -116,18 +116,15 @@ def _init_model(y, config: FitConfig, rng, eng=None) -> KruskalModel:
 
 
 def _eigh_descending(g: np.ndarray):
-    """Eigen-decomposition of a small Hermitian Gram on the GPU (cuSOLVER through torch) when
-    available; eigenvalues descending."""
-    try:
-        import torch
+    """Eigen-decomposition of a small Hermitian unfolding Gram on the GPU (cuSOLVER syevd/heevd
+    through torch -- library code, off the per-iteration path; the Gram itself is formed by the
+    engine); eigenvalues descending.  No CPU fallback: without a CUDA device this raises."""
+    import torch
 
-        if torch.cuda.is_available():
-            w, v = torch.linalg.eigh(torch.from_numpy(np.ascontiguousarray(g)).cuda())
-            w, v = w.cpu().numpy(), v.cpu().numpy()
-        else:  # pragma: no cover - the engine itself needs a GPU
-            w, v = np.linalg.eigh(g)
-    except ImportError:  # pragma: no cover
-        w, v = np.linalg.eigh(g)
+    if not torch.cuda.is_available():
+        raise RuntimeError("init='svd' needs a CUDA device (the engine has no CPU fallback)")
+    w, v = torch.linalg.eigh(torch.from_numpy(np.ascontiguousarray(g)).cuda())
+    w, v = w.cpu().numpy(), v.cpu().numpy()
     return w[::-1], v[:, ::-1]
 
 
