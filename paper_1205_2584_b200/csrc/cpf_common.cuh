@@ -198,14 +198,25 @@ struct LmDeviceState {
                              // at iteration t to force a rho > 0 / not-improved rejection
   int test_singular_iter;   // test hook (CPF_TEST_SINGULAR=t): zero a column of the core system that
                             // iteration t factors (fault injection: a zero pivot, solver.py:349-352)
-  int pad_[1];
+  int spec_iter;            // st->iter when this iteration's speculative rejection branch started
 };
 
 // Gate of the core-system kernels (Phi, LU, inverse): gate_running 0 = always, 1 = while the fit
 // runs, 2 = while it runs unless the last decision was a rho <= 0 rejection (the main core system
 // when that rejection branch was factored speculatively, engine.cu prepare_core)
+// 3 = the speculative rejection branch: as 1, and abandoned as soon as this iteration's decision is
+// an acceptance (the branch is then never used; its remaining kernels return at once and leave the
+// SMs to the accepted step's fork)
 __device__ __forceinline__ bool lu_gated(const LmDeviceState* st, int gate_running) {
-  return st && gate_running && (st->stopped || st->err_code || (gate_running == 2 && st->rej_grow));
+  return st && gate_running &&
+         (st->stopped || st->err_code || (gate_running == 2 && st->rej_grow) ||
+          (gate_running == 3 && st->iter != st->spec_iter && st->accepted));
+}
+// Kernels whose CTAs synchronise with each other (cluster panels, look-back substitutions, the
+// persistent LU) must take the same branch in every CTA; the acceptance of the running step can
+// land between two CTAs' reads, so they never abandon the speculative branch mid-way.
+__device__ __forceinline__ bool lu_gated_sync(const LmDeviceState* st, int gate_running) {
+  return lu_gated(st, gate_running == 3 ? 1 : gate_running);
 }
 
 struct IterRecordDev {

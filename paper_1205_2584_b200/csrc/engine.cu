@@ -1452,7 +1452,7 @@ struct Engine final : EngineBase {
   // errors deferred); 2: the fork's core system when a rejection branch was speculated (skipped
   // after a rejection)
   void prepare_core(int gate, int mode = 0) {
-    const int gr = mode == 2 ? 2 : (gate == kRunning ? 1 : 0);
+    const int gr = mode == 2 ? 2 : mode == 1 ? 3 : (gate == kRunning ? 1 : 0);
     if (mode == 1) {  // mu * growth snapshot: k_spec_begin on the main stream (iteration())
       launch(k_damped_inverses<T>, 2 * N, 128, 2 * R * R * sizeof(T), (const T*)Gx, N, R, Gti, Gi, st,
              (const DevFlags*)fl, gate, (const int*)nullptr, (const double*)(dscal + 8), spec_sing);
@@ -1765,7 +1765,7 @@ struct Engine final : EngineBase {
       launch(k_spec_errors, 1, 1, 0, st, (const DevFlags*)fl, (const int*)spec_sing, (const int*)luS.info);
       // this step's rejection branch, beside the candidate and pass A; its mu is snapshotted on s
       // (ordered before this iteration's k_decide), the branch itself only reads dscal[8]
-      launch(k_spec_begin, 1, 1, 0, (const LmDeviceState*)st, dscal + 8, spec_sing);
+      launch(k_spec_begin, 1, 1, 0, st, dscal + 8, spec_sing);
       CPF_CUDA_CHECK(cudaEventRecord(evS0, s));
       CPF_CUDA_CHECK(cudaStreamWaitEvent(sS, evS0, 0));
       pdl_now = false;

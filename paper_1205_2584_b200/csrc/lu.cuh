@@ -51,7 +51,7 @@ template <class T>
 __global__ void __launch_bounds__(256) k_panel_lu(T* __restrict__ A, int n, int lda, int k0, int kb, int rpc, LuWork w,
                                                   const LmDeviceState* st, int gate_running) {
   pdl_wait();
-  if (lu_gated(st, gate_running)) return;
+  if (lu_gated_sync(st, gate_running)) return;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(128) k_trsv(const T* __restrict__ A, int n, in
                                               int* __restrict__ ticket, int* __restrict__ ready, int epoch,
                                               const LmDeviceState* st, int gate_running) {
   pdl_wait();
-  if (lu_gated(st, gate_running)) return;
+  if (lu_gated_sync(st, gate_running)) return;
   __shared__ int s_b;
   __shared__ T part[4][32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;

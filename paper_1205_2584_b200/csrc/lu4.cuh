@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
                                                        T* __restrict__ invL, const LmDeviceState* st, int gate_running,
                                                        PanelPrev<T> pv) {
   pdl_wait();
-  if (lu_gated(st, gate_running)) return;
+  if (lu_gated_sync(st, gate_running)) return;
   lu_trace(0, k0 / kLuMaxKB, 0);
 #ifdef CPF_PANEL_TIMING
   const long long seg0 = clock64();

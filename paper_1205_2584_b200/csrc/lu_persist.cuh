@@ -117,7 +117,7 @@ template <class T, int NT, int RPT>
 __global__ void __launch_bounds__(NT, 1) k_lu_persist(T* A, LuPersist p, const LmDeviceState* st,
                                                       int gate_running) {
   pdl_wait();
-  if (lu_gated(st, gate_running)) return;
+  if (lu_gated_sync(st, gate_running)) return;
   constexpr int KB = kLpKB, NW = NT / 32;
   const int n = p.n, np = p.np;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;

@@ -23,6 +23,7 @@ __global__ void k_phi_assemble(T* __restrict__ Phi, int N, int R, const T* __res
   if (gate_running && st->stopped) return;
   if (st->err_code) return;
   if (gate_running == 2 && !st->accepted) return;
+  if (lu_gated(st, gate_running == 3 ? 3 : 0)) return;
   const int R2 = R * R;
   const int64_t nB = (int64_t)N * R2;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

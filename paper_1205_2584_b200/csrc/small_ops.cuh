@@ -587,10 +587,11 @@ __global__ void k_clear_pending(DevFlags* fl) {
 // Speculative rejection branch (engine.cu): mu of the branch = mu * growth, exactly k_decide's
 // rho <= 0 update; its error flags are cleared first.  Launched on the main stream BEFORE the
 // branch forks off, so the snapshot is stream-ordered ahead of this iteration's k_decide.
-__global__ void k_spec_begin(const LmDeviceState* st, double* mu_rej, int* sing) {
+__global__ void k_spec_begin(LmDeviceState* st, double* mu_rej, int* sing) {
   pdl_wait();
   *mu_rej = st->mu * st->growth;
   *sing = 0;
+  st->spec_iter = st->iter;
 }
 // After a rejection, the speculative branch's errors become the fit's (as the core system of a
 // rejected step would have reported them at the end of that step)
