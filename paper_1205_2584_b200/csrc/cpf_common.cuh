@@ -9,7 +9,16 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include <cmath>
+
+// Engine knobs: CPF_* environment variables for diagnostics, tests and A/B experiments (the full
+// list is DESIGN.md §11).  They are read only when CPF_DEBUG=1, so a production process ignores
+// stray CPF_* variables and always runs the planned paths.
+inline const char* knob(const char* name) {
+  const char* d = std::getenv("CPF_DEBUG");
+  return (d && d[0] == '1') ? std::getenv(name) : nullptr;
+}
 
 struct __align__(16) cplx {
   double x, y;
@@ -199,18 +208,21 @@ struct LmDeviceState {
   int test_singular_iter;   // test hook (CPF_TEST_SINGULAR=t): zero a column of the core system that
                             // iteration t factors (fault injection: a zero pivot, solver.py:349-352)
   int spec_iter;            // st->iter when this iteration's speculative rejection branch started
+  int accept_iter;          // t when decision t was an acceptance (else -1): ONE word, so a reader
+                            // on another SM sees the decision and its iteration together
 };
 
 // Gate of the core-system kernels (Phi, LU, inverse): gate_running 0 = always, 1 = while the fit
 // runs, 2 = while it runs unless the last decision was a rho <= 0 rejection (the main core system
 // when that rejection branch was factored speculatively, engine.cu prepare_core)
+__device__ __forceinline__ int ld_volatile_int(const int* p) { return *(const volatile int*)p; }
 // 3 = the speculative rejection branch: as 1, and abandoned as soon as this iteration's decision is
 // an acceptance (the branch is then never used; its remaining kernels return at once and leave the
 // SMs to the accepted step's fork)
 __device__ __forceinline__ bool lu_gated(const LmDeviceState* st, int gate_running) {
   return st && gate_running &&
          (st->stopped || st->err_code || (gate_running == 2 && st->rej_grow) ||
-          (gate_running == 3 && st->iter != st->spec_iter && st->accepted));
+          (gate_running == 3 && ld_volatile_int(&st->accept_iter) == st->spec_iter + 1));
 }
 // Kernels whose CTAs synchronise with each other (cluster panels, look-back substitutions, the
 // persistent LU) must take the same branch in every CTA; the acceptance of the running step can

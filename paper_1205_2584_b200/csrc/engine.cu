@@ -107,7 +107,7 @@ struct Engine final : EngineBase {
   cudaStream_t ls = nullptr;   // stream the launch helpers target (s, or s3 for the overlapped pass B)
   cudaStream_t s3 = nullptr;   // pass B + gradient of an accepted step, overlapped with the next LU
   cudaEvent_t evF = nullptr, evG = nullptr;
-  const bool serial = [] { const char* e = getenv("CPF_SERIAL"); return e && e[0] == '1'; }();
+  const bool serial = [] { const char* e = knob("CPF_SERIAL"); return e && e[0] == '1'; }();
   std::unique_ptr<Comm> comm;  // NCCL (world > 1) or the loopback test transport; null: 1 rank
   int64_t nlaunch = 0;
 
@@ -200,7 +200,7 @@ struct Engine final : EngineBase {
   double mark_ms[4] = {0, 0, 0, 0};
   // CPF_MARKS=3: the marks are external event-record nodes of the captured iteration graph, read
   // after every replay (graph-mode section times; diagnostic, one replay per poll)
-  const bool gmarks = [] { const char* e = getenv("CPF_MARKS"); return e && e[0] == '3'; }();
+  const bool gmarks = [] { const char* e = knob("CPF_MARKS"); return e && e[0] == '3'; }();
   cudaEvent_t gmark[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   bool capturing = false;
   void mark(int id) {
@@ -269,7 +269,7 @@ struct Engine final : EngineBase {
     if ((int64_t)nB * nB > (int64_t)1 << 31) throw ApiError(CPF_E_UNSUPPORTED, "N*R^2 too large");
     // CPF_FORCE_NCCL=1 runs a single-rank engine through the multi-rank code path (1-rank NCCL
     // communicator, packed allreduce / allgather / reorder kernels) so it can be tested on 1 GPU.
-    const char* fe = getenv("CPF_FORCE_NCCL");
+    const char* fe = knob("CPF_FORCE_NCCL");
     const bool force = fe && fe[0] == '1';
     if (loop) {
       // loopback test transport: P engines of one process on one GPU (comm.cuh); its host
@@ -353,7 +353,7 @@ struct Engine final : EngineBase {
     // explicit inverse pays off while its ~(4/3) n^3 flops stay below the latency of six
     // substitutions (measured: n = 1200 yes, n = 4800 no); CPF_NO_INV=1 disables
     use_inv = nB <= 2560;
-    if (const char* e = getenv("CPF_NO_INV")) if (e[0] == '1') use_inv = false;
+    if (const char* e = knob("CPF_NO_INV")) if (e[0] == '1') use_inv = false;
     if (use_inv) {
       PhiInv = dalloc<T>((size_t)nB * nB);
       TriTmp = dalloc<T>((size_t)nB * nB);
@@ -395,7 +395,7 @@ struct Engine final : EngineBase {
   int kLuReserveSms = 24;
   // pass B overlapped with the LU runs as a persistent grid on nsm - kLuReserveSms SMs, so the LU's
   // small panel clusters and GEMM updates always find free SMs (CPF_PERSISTENT_B=0: plain grid)
-  const bool persistent_b = [] { const char* e = getenv("CPF_PERSISTENT_B"); return !(e && e[0] == '0'); }();
+  const bool persistent_b = [] { const char* e = knob("CPF_PERSISTENT_B"); return !(e && e[0] == '0'); }();
   // next-block update fused into the panel load (PanelPrev, lu3.cuh): removes the gather / U12 /
   // GEMM launches between consecutive panels.  Measured (1 x B200): C1 43.3 -> 51.1 it/s, C2 359 ->
   // 405, C4 131.4 -> 131.4 (there the LU is hidden behind pass B).  CPF_LU_FUSE=0: unfused.
@@ -403,16 +403,16 @@ struct Engine final : EngineBase {
   // programmatic dependent launch for the launch() helper's kernels (CPF_PDL=0: off)
   // Only the single-stream chain from the candidate to the commit uses it: in the fork (pass B beside
   // the LU) early-scheduled CTAs would park on the SMs left to the LU (measured 162 -> 140 it/s).
-  const bool use_pdl = [] { const char* e = getenv("CPF_PDL"); return !(e && e[0] == '0'); }();
+  const bool use_pdl = [] { const char* e = knob("CPF_PDL"); return !(e && e[0] == '0'); }();
   bool pdl_now = false;
   // programmatic launch of consecutive LU panels (CPF_PDL_PANEL=1; measured no gain at C4 / C1:
   // the inter-panel gap shrinks from ~4 to ~1 us but the parked next panel slows the running one)
-  const bool pdl_panels = [] { const char* e = getenv("CPF_PDL_PANEL"); return e && e[0] == '1'; }();
+  const bool pdl_panels = [] { const char* e = knob("CPF_PDL_PANEL"); return e && e[0] == '1'; }();
   void plan() {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     nsm_ = nsm;
-    if (const char* e = getenv("CPF_LU_FUSE")) lu_fuse = e[0] == '1';
+    if (const char* e = knob("CPF_LU_FUSE")) lu_fuse = e[0] == '1';
     const size_t es = sizeof(T);
     // pass A: threads sized so 2*threads*RP*es (+W stage) fits ~160 KB
     pa_threads = 256;
@@ -460,7 +460,7 @@ struct Engine final : EngineBase {
     plan_oz();
     plan_spec();
     kLuReserveSms = use_oz ? 40 : 24;
-    if (const char* e = getenv("CPF_LU_RESERVE")) kLuReserveSms = atoi(e);
+    if (const char* e = knob("CPF_LU_RESERVE")) kLuReserveSms = atoi(e);
     CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lu_smem));
     if (lu_cl > 8) CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     set_pass_attrs();
@@ -492,7 +492,7 @@ struct Engine final : EngineBase {
     q.u12s = dalloc<T>((size_t)np * kLpKB * kLpKB);
   }
   void plan_lp() {
-    const char* e = getenv("CPF_LU");
+    const char* e = knob("CPF_LU");
     if (!(e && e[0] == '5')) return;
     if (!use_inv) return;  // the final gather uses TriTmp (allocated with the explicit inverse)
     if constexpr (sizeof(T) == 8) {
@@ -547,10 +547,13 @@ struct Engine final : EngineBase {
     CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evJ, cudaEventDisableTiming));
     for (auto& e : evB2) CPF_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     lu3_rpt = 0;
+    // CPF_PANEL_SMEM=1: the shared-memory cluster panel (lu.cuh k_panel_lu), otherwise used only
+    // when n_B exceeds 16 register-panel CTAs (n_B > 8192) -- lets the tests cover it at small n_B
+    if (const char* e = knob("CPF_PANEL_SMEM")) if (e[0] == '1') return;
     // (rows/thread, threads/CTA) candidates, smallest per-SM work first; cluster <= 16 CTAs
     const int cand[2][2] = {{1, 128}, {sizeof(T) == 8 ? 2 : 1, 256}};
     int start = 0;
-    if (const char* e = getenv("CPF_PANEL_WIDE")) if (e[0] == '1') start = 1;  // experiment knob
+    if (const char* e = knob("CPF_PANEL_WIDE")) if (e[0] == '1') start = 1;  // experiment knob
     for (int ci = start; ci < 2; ++ci) {
       const auto& c = cand[ci];
       if ((nB + c[0] * c[1] - 1) / (c[0] * c[1]) <= 16) { lu3_rpt = c[0]; lu3_thr = c[1]; break; }
@@ -559,7 +562,7 @@ struct Engine final : EngineBase {
     // the rotating-frame panel wins from n_B ~ 1000 up (config 4: 1200, config 1: 4800; measured
     // slower at 300 / 900), and its 2-3 CTA clusters co-schedule next to the persistent pass B
     use_lu4 = nB > 1024 && (nB + kLu4Rpt * kLu4Thr - 1) / (kLu4Rpt * kLu4Thr) <= 16;
-    if (const char* e = getenv("CPF_PANEL_V3")) if (e[0] == '1') use_lu4 = false;
+    if (const char* e = knob("CPF_PANEL_V3")) if (e[0] == '1') use_lu4 = false;
     if (use_lu4) {
       const size_t smem = panel4_smem_bytes<T>(16, kLu4Thr, kLu4Rpt);
       CPF_CUDA_CHECK(cudaFuncSetAttribute(k_panel_lu4<T, kLu4Rpt, kLu4Thr>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -644,7 +647,7 @@ struct Engine final : EngineBase {
     use_oz = false;
     if constexpr (sizeof(T) != 8) return;
     else {
-      const char* e = getenv("CPF_OZ");
+      const char* e = knob("CPF_OZ");
       const bool force = e && e[0] == '1';
       if (e && e[0] == '0') return;
       // int32 accumulators: 8 pairs x 127^2 per K element -> K <= 16384 per contraction
@@ -655,7 +658,7 @@ struct Engine final : EngineBase {
       ob = OzGeom{I1, Lmid, Cloc, nb, (int)((Lmid + kOzK - 1) / kOzK), Cloc, (int64_t)nb * Cloc, R, 0};
       // pass A streams alone: no L2 hint (measured 3 % faster); pass B runs beside the LU: evict-first
       oa.dbg = 4;
-      if (const char* d = getenv("CPF_OZ_DBG")) oa.dbg = ob.dbg = atoi(d);  // experiments
+      if (const char* d = knob("CPF_OZ_DBG")) oa.dbg = ob.dbg = atoi(d);  // experiments
       // the two digit-plane images (~2 x 8 B per element) must fit next to everything else with
       // 2 GB to spare; otherwise stay on the fp64 DMMA passes
       const size_t need = ((size_t)oa.ntiles * oa.nkb + (size_t)ob.ntiles * ob.nkb) * kOzABytes;
@@ -693,7 +696,7 @@ struct Engine final : EngineBase {
   // steps than the skipped LU saves: 157.7 -> 151.7 it/s).  CPF_SPEC=0/1 overrides.
   void plan_spec() {
     use_spec = use_inv && lu3_rpt && !use_oz && !use_dmma;
-    if (const char* e = getenv("CPF_SPEC")) use_spec = e[0] == '1' && use_inv && lu3_rpt;
+    if (const char* e = knob("CPF_SPEC")) use_spec = e[0] == '1' && use_inv && lu3_rpt;
     if (!use_spec) return;
     const size_t R2 = (size_t)R * R;
     PhiS = dalloc<T>((size_t)nB * nB);
@@ -763,7 +766,7 @@ struct Engine final : EngineBase {
         CPF_CUDA_CHECK(cudaFreeAsync(ozYB, s));
         ozYA = ozYB = nullptr;
         kLuReserveSms = 24;
-        if (const char* e = getenv("CPF_LU_RESERVE")) kLuReserveSms = atoi(e);
+        if (const char* e = knob("CPF_LU_RESERVE")) kLuReserveSms = atoi(e);
         return;
       }
       k_oz_split_y<0><<<nsm_ * 16, 256, 0, s>>>(Yd, oa, ozFrowA, ozYA);
@@ -777,7 +780,7 @@ struct Engine final : EngineBase {
     if constexpr (sizeof(T) != 8) return;
     else {
       if (I1 < 256 || I1 % 2 != 0 || Cloc < 1) return;
-      if (const char* e = getenv("CPF_NO_DMMA")) if (e[0] == '1') return;
+      if (const char* e = knob("CPF_NO_DMMA")) if (e[0] == '1') return;
       dm_nt = (R + 7) / 8;
       if (dm_nt == 7) dm_nt = 8;
       int ws = 8 * dm_nt;
@@ -1725,13 +1728,13 @@ struct Engine final : EngineBase {
       const double pass_flops = 2.0 * cw * (double)Lrows * IN * R;
       const double lu_flops = (2.0 / 3.0) * cw * (double)nB * nB * nB;
       hst->force_direct = pass_flops < 0.05 * lu_flops ? 1 : 0;
-      if (const char* e = getenv("CPF_FORCE_DIRECT")) hst->force_direct = (e[0] == '1');
+      if (const char* e = knob("CPF_FORCE_DIRECT")) hst->force_direct = (e[0] == '1');
     }
     hst->rej_grow = 0;
     hst->test_negdenom_iter = 0;
-    if (const char* e = getenv("CPF_TEST_NEGDENOM")) hst->test_negdenom_iter = atoi(e);  // test hook
+    if (const char* e = knob("CPF_TEST_NEGDENOM")) hst->test_negdenom_iter = atoi(e);  // test hook
     hst->test_singular_iter = 0;
-    if (const char* e = getenv("CPF_TEST_SINGULAR")) hst->test_singular_iter = atoi(e);  // test hook
+    if (const char* e = knob("CPF_TEST_SINGULAR")) hst->test_singular_iter = atoi(e);  // test hook
     if (test_singular != (hst->test_singular_iter != 0) && gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
     test_singular = hst->test_singular_iter != 0;
     // keep use_kinv computed by the cache kernels
@@ -1852,7 +1855,7 @@ struct Engine final : EngineBase {
 
   void fit_step(int n, cpf_status* o) override {
     pull_state();
-    const char* env = getenv("CPF_NO_GRAPH");
+    const char* env = knob("CPF_NO_GRAPH");
     const bool use_graph = graph_ok && !prof && !(env && env[0] == '1');
     if (use_graph && !gexec) capture_iteration();
     int k = 0;
@@ -1949,7 +1952,7 @@ struct Engine final : EngineBase {
       cudaEventDestroy(e.b);
     }
     evs.clear();
-    const bool verbose = getenv("CPF_MARKS") && getenv("CPF_MARKS")[0] == '2';
+    const bool verbose = knob("CPF_MARKS") && knob("CPF_MARKS")[0] == '2';
     for (size_t i = 0; i + 1 < marks.size(); ++i) {
       const int a = marks[i].first, b = marks[i + 1].first;
       if (b == a + 1 && a < 4) {
@@ -1961,7 +1964,7 @@ struct Engine final : EngineBase {
     }
     for (auto& m : marks) cudaEventDestroy(m.second);
     marks.clear();
-    if (const char* e = getenv("CPF_MARKS"))
+    if (const char* e = knob("CPF_MARKS"))
       if (e[0] == '1')
         fprintf(stderr, "[cpf marks] candidate %.3f  passA+decide %.3f  commit %.3f  fork %.3f ms (totals)\n",
                 mark_ms[0], mark_ms[1], mark_ms[2], mark_ms[3]);

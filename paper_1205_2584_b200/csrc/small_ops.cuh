@@ -697,6 +697,7 @@ __global__ void k_decide(LmDeviceState* st, DevFlags* fl, IterRecordDev* trace, 
   }
   st->cand_zero = 0;
   st->accepted = acc;
+  st->accept_iter = acc ? t : -1;
   st->rej_grow = ok ? 0 : 1;
   st->deltas[st->ndeltas % 10] = d;
   st->ndeltas += 1;

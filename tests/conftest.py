@@ -1,7 +1,12 @@
+import os
 import sys
 from pathlib import Path
 
 import pytest
+
+# the tests steer the engine through its CPF_* knobs (pass families, schedules, fault injection),
+# which the engine reads only under CPF_DEBUG=1 (cpf_common.cuh knob())
+os.environ.setdefault("CPF_DEBUG", "1")
 
 ROOT = Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:

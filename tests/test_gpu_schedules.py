@@ -64,3 +64,13 @@ def test_bitwise_identical_across_schedules(api, monkeypatch, case):
         tr, v = _run(api, monkeypatch, case, env)
         assert tr == base_tr, f"trace differs under {env}"
         assert np.array_equal(v, base_v), f"factors differ under {env}: max |d| {np.max(np.abs(v - base_v)):.3e}"
+
+
+@pytest.mark.parametrize("case", ["c0", "c2mini", "c3mini"])
+def test_repeated_fits_bitwise(api, monkeypatch, case):
+    """Ten repeats with the speculative rejection branch on (its early abandonment reads the
+    decision written by another stream's kernel: a torn read once made ~1 in 6 runs diverge)."""
+    base_tr, base_v = _run(api, monkeypatch, case, {"CPF_SPEC": "1"})
+    for _ in range(9):
+        tr, v = _run(api, monkeypatch, case, {"CPF_SPEC": "1"})
+        assert tr == base_tr and np.array_equal(v, base_v)

@@ -1,5 +1,7 @@
 """Per-iteration section times of a config-4 fit: eager, profiled (CPF_MARKS=2) or graph replay (CPF_MARKS=3):
 candidate | normalise + pass A + trial fit + decide | commit | fork (pass B || next core) -> join."""
+import os as _os
+_os.environ.setdefault("CPF_DEBUG", "1")  # engine knobs are read only under CPF_DEBUG=1
 import os
 import sys
 

@@ -4,6 +4,8 @@ helpers' look-ahead task [first start, last end], in us from the first step; plu
 of eagerly launched iterations.  Usage: python tools/lp_timeline.py [N R]  (default 3 20 ->
 n_B = 1200, the config-4 core system; the tensor is a small random one: the LU does not depend
 on it)."""
+import os as _os
+_os.environ.setdefault("CPF_DEBUG", "1")  # engine knobs are read only under CPF_DEBUG=1
 import ctypes
 import os
 import sys

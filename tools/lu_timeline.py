@@ -1,6 +1,8 @@
 """LU timeline of one config-4 iteration in graph replay (cpf_debug_lu_trace): per panel step the
 start/end of the panel kernel (stream s) and of the trailing U12 / GEMM (stream s2), in us from
 the first panel's start."""
+import os as _os
+_os.environ.setdefault("CPF_DEBUG", "1")  # engine knobs are read only under CPF_DEBUG=1
 import ctypes
 import os
 import sys

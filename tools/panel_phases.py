@@ -1,5 +1,7 @@
 """Per-column phase cycles of the LU panel (build with CPF_NVCC_DEFS=-DCPF_PANEL_TIMING): CTA 0,
 thread 0, summed over all panels of the run, divided by the columns processed."""
+import os as _os
+_os.environ.setdefault("CPF_DEBUG", "1")  # engine knobs are read only under CPF_DEBUG=1
 import ctypes
 import os
 import sys

@@ -4,6 +4,8 @@ rank runs -- minus the two NCCL collectives per iteration (a 320 KB allreduce + 
 allgather, ~10-30 us over NVLink 5).  Times are device time per iteration over 20 graph replays
 after 3 warm-up iterations.  The slab's own accept/reject pattern differs from the full problem's,
 so this bounds the per-rank cost, it is not a scaling measurement."""
+import os as _os
+_os.environ.setdefault("CPF_DEBUG", "1")  # engine knobs are read only under CPF_DEBUG=1
 import os
 import sys
 

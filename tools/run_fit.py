@@ -1,4 +1,6 @@
 """Run a short fit on a BASELINE config (device-generated tensor) -- for ncu / nsight captures."""
+import os as _os
+_os.environ.setdefault("CPF_DEBUG", "1")  # engine knobs are read only under CPF_DEBUG=1
 import sys, numpy as np
 sys.path.insert(0, '.')
 import torch

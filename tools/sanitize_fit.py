@@ -2,6 +2,8 @@
 C2 mini (4-way, 12^4, R=5) through the public fit(), graph replay and eager (CPF_NO_GRAPH=1)
 modes chosen by the caller's environment, plus the int8 passes (CPF_OZ=1) when asked.
 Usage: compute-sanitizer --tool racecheck python tools/sanitize_fit.py [c0|c2mini|c3mini|als]"""
+import os as _os
+_os.environ.setdefault("CPF_DEBUG", "1")  # engine knobs are read only under CPF_DEBUG=1
 
 import sys
 from pathlib import Path
