@@ -1,5 +1,12 @@
 // LU v4 panel: k_panel_lu4 -- register-resident m x 32 panel with a ROTATING register frame.
 //
+// Round 2: the frame now rotates by ONE column per column (CH = 1).  With 8-column unrolled chunks
+// the column loop was ~80 KB of SASS and ncu showed no_instructions as the top stall (29-40 %);
+// the 31 register moves of a per-column shift cost less than the instruction-cache misses:
+// measured (1 x B200, bench.py, same box) LU phase config 4 2.38-2.43 -> 2.24-2.25 ms, 164-166 ->
+// 168-170 it/s; config 1 (n_B = 4800) LU 9.44 -> 8.53 ms, 57.5 -> 62.6 it/s (CH = 2 and 4 in
+// between).
+//
 // Same algorithm and interface as k_panel_lu3 (lu3.cuh): partial pivoting by |a| (|re|+|im| for
 // complex, LAPACK's cabs1), ties to the smaller row, pivot rows retired logically and written
 // once at the end, interchange emitted as a gather list, inv(L11) for k_u12.  What changes is
@@ -53,7 +60,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
   const long long seg0 = clock64();
 #endif
   constexpr int KB = kLuMaxKB;  // 32
-  constexpr int CH = 8;         // columns per static chunk
+  constexpr int CH = 1;         // columns per static chunk (see the header: 1 is fastest)
   constexpr int NW = NTHR / 32;
   constexpr int ROWS = RPT * NTHR;  // rows per CTA
   using PK = PanelPacket<T, KB>;
@@ -133,7 +140,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
     for (int u = 0; u < CH; ++u) {
       const int jj = c8 + u;
       if (jj >= kb) break;
-      const int par = u & 1;  // == jj & 1 (c8 is a multiple of 8)
+      const int par = jj & 1;
       const double wv = nwv;
       const int wrow = nwrow, wlane = nwlane, bj = nbj;
       PT(0);
