@@ -315,7 +315,7 @@ struct Engine final : EngineBase {
                     norms, dscal, red, ibuf, st, fl, dtrace, kinv_ok, invL, WNd, KMd, gring, PhiInv, TriTmp, yvec, tmv_part,
                     ozYA, ozYB, ozBA, ozBB, ozFrowA, ozFrowB, ozFr, ozM1, ozZ, ozBp,
                     PhiS, PhiInvS, TriTmpS, GtiS, GiS, invLS, ibufS, gringS, spec_sing, Hist, Pinv,
-                    lp.panel_done, lp.u12s, lpS.panel_done, lpS.u12s};
+                    lp.panel_done, lp.u12s, lpS.panel_done, lpS.u12s, TriPart, TriPartS};
     for (void* p : ptrs)
       if (p) cudaFreeAsync(p, s);  // back to the device pool (kept for the next engine)
     if (hst) cudaFreeHost(hst);
@@ -357,6 +357,7 @@ struct Engine final : EngineBase {
     if (use_inv) {
       PhiInv = dalloc<T>((size_t)nB * nB);
       TriTmp = dalloc<T>((size_t)nB * nB);
+      if (nB > 256) TriPart = dalloc<T>((size_t)kTriSplit * nB * nB);
       yvec = dalloc<T>(nB);
       tmv_part = dalloc<T>((size_t)((nB + kTmvCols - 1) / kTmvCols) * nB);
     }
@@ -702,6 +703,7 @@ struct Engine final : EngineBase {
     PhiS = dalloc<T>((size_t)nB * nB);
     PhiInvS = dalloc<T>((size_t)nB * nB);
     TriTmpS = dalloc<T>((size_t)nB * nB);
+    if (nB > 256) TriPartS = dalloc<T>((size_t)kTriSplit * nB * nB);
     GtiS = dalloc<T>(N * R2);
     GiS = dalloc<T>(N * R2);
     invLS = dalloc<T>(2 * kLuMaxKB * kLuMaxKB);
@@ -733,6 +735,7 @@ struct Engine final : EngineBase {
     std::swap(Phi, PhiS);
     std::swap(PhiInv, PhiInvS);
     std::swap(TriTmp, TriTmpS);
+    std::swap(TriPart, TriPartS);
     std::swap(Gti, GtiS);
     std::swap(Gi, GiS);
     std::swap(invL, invLS);
@@ -1400,17 +1403,34 @@ struct Engine final : EngineBase {
   }
   // f = B w  (flm-b: Phi^{-1} w; flm-a: K Phi^{-1} w)
   // inv(L), inv(U) of the factored Phi (tri_inv.cuh), packed like the factors
+  // split-K factor of a triangular-inverse level (levels with few output tiles and long K)
+  int tri_split(int sz) const {
+    int k = kTriSplit;
+    if (const char* e = knob("CPF_TRI_SPLIT")) k = std::max(1, std::min(kTriSplit, atoi(e)));
+    return sz >= 256 ? k : 1;
+  }
+  static constexpr int kTriSplit = 4;
+  T* TriPart = nullptr;   // split-K partials: kTriSplit x nB x nB
+  T* TriPartS = nullptr;  // the speculative branch's
   void tri_invert(int gate_running) {
     ph_begin(kPhLU);
     const int nblk = (nB + 31) / 32;
     launch(k_tri_inv_diag<T>, nblk, 64, 0, (const T*)Phi, nB, PhiInv, (const LmDeviceState*)st, gate_running);
     for (int sz = 32; sz < nB; sz *= 2) {
       const int npairs = (nB + 2 * sz - 1) / (2 * sz);
-      const dim3 grid((sz + 63) / 64, (sz + 63) / 64, 2 * npairs);
+      const int ks = tri_split(sz);
+      const dim3 grid((sz + 63) / 64, (sz + 63) / 64, 2 * npairs * ks);
+      const dim3 rgrid(std::max(1, std::min(256, (int)nblocks((int64_t)sz * sz, 256))), 2 * npairs);
       launch(k_tri_level<T, 0>, grid, 256, 0, (const T*)Phi, PhiInv, TriTmp, nB, sz, (const LmDeviceState*)st,
-             gate_running);
+             gate_running, ks, ks > 1 ? TriPart : (T*)nullptr);
+      if (ks > 1)
+        launch(k_tri_reduce<T, 0>, rgrid, 256, 0, PhiInv, TriTmp, (const T*)TriPart, ks, nB, sz, (const LmDeviceState*)st,
+               gate_running);
       launch(k_tri_level<T, 1>, grid, 256, 0, (const T*)Phi, PhiInv, TriTmp, nB, sz, (const LmDeviceState*)st,
-             gate_running);
+             gate_running, ks, ks > 1 ? TriPart : (T*)nullptr);
+      if (ks > 1)
+        launch(k_tri_reduce<T, 1>, rgrid, 256, 0, PhiInv, TriTmp, (const T*)TriPart, ks, nB, sz, (const LmDeviceState*)st,
+               gate_running);
     }
     ph_end();
   }

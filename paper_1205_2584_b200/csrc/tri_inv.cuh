@@ -77,15 +77,22 @@ __device__ __forceinline__ T tri_elem(const T* M, int n, int r, int c, int kind)
 }
 
 // One level product for every (pair, triangle): C = alpha * opA(A) * opB(B), all blocks inside
-// n x n column-major matrices.  blockIdx.z = 2 * pair + tri (tri 0: L, 1: U).
+// n x n column-major matrices.  blockIdx.z = (2 * pair + tri) * ksplit + ks (tri 0: L, 1: U).
+// Split-K (ksplit > 1, the large levels): split ks covers its share of the (triangle-skipped) K
+// range and writes alpha * partial into part[ks] (n x n layout); k_tri_reduce adds the ksplit
+// partials in fixed order -- deterministic.  The large levels have few output tiles and K up to
+// n: without the split a handful of CTAs run 1024-deep K loops (ncu: ~100 us per launch at
+// n_B = 1200, issue 18-22 %).
 //   step 0 (T):  L: T[b2,b1] = L21 * inv(L11)      U: T[b1,b2] = U12 * inv(U22)
 //   step 1 (X):  L: X[b2,b1] = -inv(L22) * T        U: X[b1,b2] = -inv(U11) * T
 template <class T, int STEP>
 __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* __restrict__ Inv, T* __restrict__ Tmp,
-                                                   int n, int s, const LmDeviceState* st, int gate_running) {
+                                                   int n, int s, const LmDeviceState* st, int gate_running,
+                                                   int ksplit = 1, T* __restrict__ part = nullptr) {
   pdl_wait();
   if (lu_gated(st, gate_running)) return;
-  const int pair = blockIdx.z >> 1, tri = blockIdx.z & 1;
+  const int ks = blockIdx.z % ksplit, pt = blockIdx.z / ksplit;
+  const int pair = pt >> 1, tri = pt & 1;
   const int b1 = 2 * pair * s, b2 = b1 + s;
   if (b2 >= n) return;
   const int s1 = s, s2 = min(s, n - b2);
@@ -115,6 +122,15 @@ __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* 
   if (kindB == kOpInvL) kbeg = max(kbeg, tn);        // col j needs k >= j
   if (kindB == kOpInvU) kend = min(kend, tn + 64);   // col j needs k <= j
   kbeg &= ~(KS - 1);
+  if (ksplit > 1) {  // this split's share of [kbeg, kend), in whole K slabs
+    const int per = ((max(kend - kbeg, 0) + ksplit - 1) / ksplit + KS - 1) / KS * KS;
+    const int lo = kbeg + ks * per;
+    kend = min(kend, lo + per);
+    kbeg = lo;
+  }
+  if (ksplit > 1) {
+    Cm = part + (size_t)ks * n * n;
+  }
   __shared__ T As[2][KS][64 + 1];
   __shared__ T Bs[2][KS][64 + 1];
   const int tid = threadIdx.x;
@@ -221,6 +237,30 @@ __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* 
         const int r = tm + tx + 16 * i, c = tn + ty + 16 * j;
         if (r < m && c < nn) Cm[(int64_t)(rc + r) + (int64_t)n * (cc + c)] = scale(acc[i][j], alpha);
       }
+  }
+}
+
+// Sum of the split-K partials of one level (fixed order) into its output blocks: STEP 0 -> Tmp,
+// STEP 1 -> Inv.  grid.y = 2 * npairs (pair, triangle).
+template <class T, int STEP>
+__global__ void k_tri_reduce(T* __restrict__ Inv, T* __restrict__ Tmp, const T* __restrict__ part, int ksplit, int n,
+                             int s, const LmDeviceState* st, int gate_running) {
+  pdl_wait();
+  if (lu_gated(st, gate_running)) return;
+  const int pair = blockIdx.y >> 1, tri = blockIdx.y & 1;
+  const int b1 = 2 * pair * s, b2 = b1 + s;
+  if (b2 >= n) return;
+  const int s1 = s, s2 = min(s, n - b2);
+  const int rc = tri == 0 ? b2 : b1, cc = tri == 0 ? b1 : b2;
+  const int m = tri == 0 ? s2 : s1, nn = tri == 0 ? s1 : s2;
+  T* dst = STEP == 0 ? Tmp : Inv;
+  const size_t nn2 = (size_t)n * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)m * nn; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % m), c = (int)(e / m);
+    const size_t off = (size_t)(rc + r) + (size_t)n * (cc + c);
+    T v = part[off];
+    for (int k = 1; k < ksplit; ++k) v = add(v, part[(size_t)k * nn2 + off]);
+    dst[off] = v;
   }
 }
 
