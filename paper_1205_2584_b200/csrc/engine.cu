@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -55,6 +56,41 @@ struct ApiError : std::runtime_error {
 #include "comm.cuh"
 
 namespace cpf {
+
+// Process-wide cache of tensor-sized device buffers (see Engine::big_alloc): exact-size reuse
+// (the next engine of the same problem asks for the same sizes), released on allocation failure.
+struct BigCache {
+  struct Buf { int dev; size_t bytes; void* p; };
+  static std::mutex& mu() { static std::mutex m; return m; }
+  static std::vector<Buf>& bufs() { static std::vector<Buf> v; return v; }
+  static void* take(int dev, size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu());
+    auto& v = bufs();
+    for (size_t i = 0; i < v.size(); ++i)
+      if (v[i].dev == dev && v[i].bytes == bytes) {
+        void* p = v[i].p;
+        v.erase(v.begin() + (long)i);
+        return p;
+      }
+    return nullptr;
+  }
+  static void park(int dev, void* p, size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu());
+    bufs().push_back({dev, bytes, p});
+  }
+  static void release(int dev) {
+    std::lock_guard<std::mutex> lk(mu());
+    auto& v = bufs();
+    for (size_t i = 0; i < v.size();) {
+      if (v[i].dev == dev) {
+        cudaFree(v[i].p);
+        v.erase(v.begin() + (long)i);
+      } else {
+        ++i;
+      }
+    }
+  }
+};
 
 static int padded_rank(int R) {
   static const int table[] = {2, 4, 6, 8, 10, 12, 16, 20, 24, 32, 40, 48, 64};  // even: paired smem loads
@@ -317,7 +353,11 @@ struct Engine final : EngineBase {
                     PhiS, PhiInvS, TriTmpS, GtiS, GiS, invLS, ibufS, gringS, spec_sing, Hist, Pinv,
                     lp.panel_done, lp.u12s, lpS.panel_done, lpS.u12s, TriPart, TriPartS};
     for (void* p : ptrs)
-      if (p) cudaFreeAsync(p, s);  // back to the device pool (kept for the next engine)
+      if (p && std::find_if(big_bufs.begin(), big_bufs.end(), [&](const auto& b) { return b.first == p; }) ==
+                   big_bufs.end())
+        cudaFreeAsync(p, s);  // back to the device pool (kept for the next engine)
+    if (s) cudaStreamSynchronize(s);  // every stream of the engine joins s: nothing uses them now
+    for (const auto& b : big_bufs) BigCache::park(dev, b.first, b.second);
     if (hst) cudaFreeHost(hst);
     comm.reset();
     if (s) cudaStreamDestroy(s);
@@ -332,6 +372,44 @@ struct Engine final : EngineBase {
     if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
     uint64_t thr = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  // Tensor-sized buffers (the bound slab, the int8 digit-plane images: ~50 GB at config 4) come
+  // from cudaMalloc, not the stream-ordered pool: growing the pool by that much costs ~0.9 s on
+  // the first fit of a process (measured: cpf_pool_reserve of 50 GB 300 ms, a cold fit() 1.16 s
+  // for engine + upload vs 0.30 s warm), cudaMalloc of 16 GB ~3-6 ms.  A destroyed engine parks
+  // them in a process-wide cache (BigCache) for the next engine -- as the pool did, without the
+  // pool's growth cost -- instead of cudaFree (~0.1 s for 50 GB, on every fit).
+  static constexpr size_t kBigAlloc = (size_t)1 << 30;
+  std::vector<std::pair<void*, size_t>> big_bufs;
+  void* big_alloc(size_t bytes, bool zero) {
+    if (bytes < kBigAlloc || knob("CPF_POOL_ONLY")) {
+      void* p = nullptr;
+      CPF_CUDA_CHECK(cudaMallocAsync(&p, std::max<size_t>(bytes, 1), s));
+      if (zero) CPF_CUDA_CHECK(cudaMemsetAsync(p, 0, std::max<size_t>(bytes, 1), s));
+      return p;
+    }
+    void* p = BigCache::take(dev, bytes);
+    if (!p) {
+      cudaError_t e = cudaMalloc(&p, bytes);
+      if (e == cudaErrorMemoryAllocation) {  // release what earlier engines parked and retry
+        cudaGetLastError();
+        BigCache::release(dev);
+        e = cudaMalloc(&p, bytes);
+      }
+      CPF_CUDA_CHECK(e);
+    }
+    big_bufs.push_back({p, bytes});
+    if (zero) CPF_CUDA_CHECK(cudaMemsetAsync(p, 0, bytes, s));
+    return p;
+  }
+  void big_free(void* p) {
+    if (!p) return;
+    auto it = std::find_if(big_bufs.begin(), big_bufs.end(), [&](const auto& b) { return b.first == p; });
+    if (it == big_bufs.end()) { CPF_CUDA_CHECK(cudaFreeAsync(p, s)); return; }
+    const size_t bytes = it->second;
+    big_bufs.erase(it);
+    CPF_CUDA_CHECK(cudaStreamSynchronize(s));
+    BigCache::park(dev, p, bytes);
   }
   template <class U>
   U* dalloc(size_t n) {
@@ -676,8 +754,8 @@ struct Engine final : EngineBase {
           free_b += (size_t)(reserved - used);
       }
       if (!force && need + ((size_t)2 << 30) + (size_t)Jloc * sizeof(T) > free_b) return;
-      ozYA = dalloc<uint8_t>((size_t)oa.ntiles * oa.nkb * kOzABytes);
-      ozYB = dalloc<uint8_t>((size_t)ob.ntiles * ob.nkb * kOzABytes);
+      ozYA = static_cast<uint8_t*>(big_alloc((size_t)oa.ntiles * oa.nkb * kOzABytes, true));
+      ozYB = static_cast<uint8_t*>(big_alloc((size_t)ob.ntiles * ob.nkb * kOzABytes, true));
       ozFrowA = dalloc<int>((size_t)oa.ntiles * kOzM);
       ozFrowB = dalloc<int>((size_t)ob.ntiles * kOzM);
       ozBA = dalloc<uint8_t>((size_t)oa.nkb * kOzBBytes);  // zero: padding columns / K tail
@@ -765,8 +843,8 @@ struct Engine final : EngineBase {
       if (nbad > 0) {
         oz_y_rejected = true;
         use_oz = false;
-        CPF_CUDA_CHECK(cudaFreeAsync(ozYA, s));
-        CPF_CUDA_CHECK(cudaFreeAsync(ozYB, s));
+        big_free(ozYA);
+        big_free(ozYB);
         ozYA = ozYB = nullptr;
         kLuReserveSms = 24;
         if (const char* e = knob("CPF_LU_RESERVE")) kLuReserveSms = atoi(e);
@@ -1609,14 +1687,10 @@ struct Engine final : EngineBase {
     CPF_CUDA_CHECK(cudaSetDevice(dev));
     if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }  // Y pointer is baked into the graph
     if (where == 1) {
-      if (Yown) { CPF_CUDA_CHECK(cudaFreeAsync(Yown, s)); Yown = nullptr; }
+      if (Yown) { big_free(Yown); Yown = nullptr; }
       Y = static_cast<const T*>(p);
     } else {
-      if (!Yown) {
-        void* q = nullptr;
-        CPF_CUDA_CHECK(cudaMallocAsync(&q, std::max<int64_t>(Jloc, 1) * sizeof(T), s));
-        Yown = static_cast<T*>(q);
-      }
+      if (!Yown) Yown = static_cast<T*>(big_alloc((size_t)std::max<int64_t>(Jloc, 1) * sizeof(T), false));
       if (Jloc > 0) CPF_CUDA_CHECK(cudaMemcpyAsync(Yown, p, Jloc * sizeof(T), cudaMemcpyHostToDevice, s));
       Y = Yown;
     }
@@ -1639,11 +1713,7 @@ struct Engine final : EngineBase {
     if ((int64_t)sb.st_size < payload_off || have != count || ((int64_t)sb.st_size - payload_off) % es != 0)
       throw ApiError(CPF_E_FORMAT, "expected " + std::to_string(count) + " scalars, found " + std::to_string(have));
     posix_fadvise(fd, 0, 0, POSIX_FADV_SEQUENTIAL);
-    if (!Yown) {
-      void* q = nullptr;
-      CPF_CUDA_CHECK(cudaMallocAsync(&q, std::max<int64_t>(Jloc, 1) * sizeof(T), s));
-      Yown = static_cast<T*>(q);
-    }
+    if (!Yown) Yown = static_cast<T*>(big_alloc((size_t)std::max<int64_t>(Jloc, 1) * sizeof(T), false));
     const int64_t bytes = Jloc * es;
     const int64_t start = payload_off + slab_lo * Lrows * es;
     const int64_t chunk = std::min<int64_t>(bytes, (int64_t)64 << 20);
