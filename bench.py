@@ -282,9 +282,10 @@ def main():
     tau = synth.tau_for_unit_mu(cfg, args.seed)
     K, W = args.steps, args.warmup
 
-    # ---- end to end through the public API, tensor in pinned HOST memory.  Run first, in a process
-    # whose engine memory pool is still empty: the cold call pays the pool's first-time mapping of the
-    # fit's ~50 GB; the warm call (after the device-resident timing) is a long-lived process's fit().
+    # ---- end to end through the public API, tensor in pinned HOST memory.  Run first, in a fresh
+    # process: the cold call allocates the fit's ~50 GB (tensor + int8 images, cudaMalloc); the warm
+    # call (after the device-resident timing) is a long-lived process's fit(), reusing the buffers
+    # an earlier engine parked in the engine's buffer cache.
     y_host = None
     e2e_runs = {}
 
@@ -427,8 +428,8 @@ def main():
                "cold_value": v_cold,
                "what": "public fit() from pinned host memory: H2D of the tensor slab, preamble, "
                        f"{res.iters} iterations, factor download; wall clock max over ranks.  value: a process "
-                       "whose engine memory pool already holds the fit's footprint (an earlier fit); cold_value: "
-                       "the first fit() of the process (pool grows by the tensor + int8 images inside the call)"}
+                       "that has run a fit before (its tensor-sized buffers are reused from the engine's buffer "
+                       "cache); cold_value: the first fit() of the process (allocates them inside the call)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
