@@ -55,6 +55,16 @@ struct ApiError : std::runtime_error {
 
 #include "comm.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX ranges on the host orchestration (SURVEY §5 tracing): what an nsys / ncu --nvtx timeline
+// groups by.  Inside a captured iteration they mark the capture; graph replays are marked by
+// fit_step's range.  Header-only NVTX3: no library dependency, no cost without a profiler.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 namespace cpf {
 
 // Process-wide cache of tensor-sized device buffers (see Engine::big_alloc): exact-size reuse
@@ -829,6 +839,7 @@ struct Engine final : EngineBase {
   // split's envelope, the engine drops the int8 passes for this tensor and stays on fp64.
   bool oz_y_rejected = false;
   void oz_split() {
+    NvtxRange nvtx_("cpf.oz_split (int8 digit-plane images)");
     if (!use_oz || Jloc == 0) return;
     if constexpr (sizeof(T) == 8) {
       const double* Yd = reinterpret_cast<const double*>(Y);
@@ -1085,6 +1096,7 @@ struct Engine final : EngineBase {
   // Int8 (Ozaki) passes: the operand split also checks the accuracy envelope; the int8 kernels are
   // gated on it and the fp64 pass below runs instead when the operand is outside it.
   void pass_a(const T* F, T* Mout, int gate) {
+    NvtxRange nvtx_("cpf.pass_a");
     prep_operands(F, true, gate);
     ph_begin(kPhPassA);
     bool oz = false;
@@ -1178,6 +1190,7 @@ struct Engine final : EngineBase {
 
   // Pass B at factors F -> mode N of Mout (allgathered).  Int8 passes: guarded like pass A.
   void pass_b(const T* F, T* Mout, int gate) {
+    NvtxRange nvtx_("cpf.pass_b");
     prep_operands(F, false, gate);
     ph_begin(kPhPassB);
     struct Red { const T* src; int nparts; int gate; };
@@ -1377,6 +1390,7 @@ struct Engine final : EngineBase {
   }
 
   void lu_factor(int gate_running) {
+    NvtxRange nvtx_("cpf.lu");
     ph_begin(kPhLU);
     if (lp_cfg) {
       lu_factor_lp(gate_running);
@@ -1491,6 +1505,7 @@ struct Engine final : EngineBase {
   T* TriPart = nullptr;   // split-K partials: kTriSplit x nB x nB
   T* TriPartS = nullptr;  // the speculative branch's
   void tri_invert(int gate_running) {
+    NvtxRange nvtx_("cpf.tri_inverse");
     ph_begin(kPhLU);
     const int nblk = (nB + 31) / 32;
     launch(k_tri_inv_diag<T>, nblk, 64, 0, (const T*)Phi, nB, PhiInv, (const LmDeviceState*)st, gate_running);
@@ -1553,6 +1568,7 @@ struct Engine final : EngineBase {
   // errors deferred); 2: the fork's core system when a rejection branch was speculated (skipped
   // after a rejection)
   void prepare_core(int gate, int mode = 0) {
+    NvtxRange nvtx_("cpf.core_system (phi + lu + inverse)");
     const int gr = mode == 2 ? 2 : mode == 1 ? 3 : (gate == kRunning ? 1 : 0);
     if (mode == 1) {  // mu * growth snapshot: k_spec_begin on the main stream (iteration())
       launch(k_damped_inverses<T>, 2 * N, 128, 2 * R * R * sizeof(T), (const T*)Gx, N, R, Gti, Gi, st,
@@ -1573,6 +1589,7 @@ struct Engine final : EngineBase {
   }
 
   void candidate(int refine_steps, int gate, bool core_ready = false) {
+    NvtxRange nvtx_("cpf.candidate");
     const int gr = gate == kRunning ? 1 : 0;
     if (!core_ready) prepare_core(gate);
     // damped factors D = M Gti
@@ -1683,6 +1700,7 @@ struct Engine final : EngineBase {
   void* stream() override { return (void*)s; }
 
   void set_tensor(const void* p, int64_t n, int where) override {
+    NvtxRange nvtx_("cpf.set_tensor (upload)");
     if (n != Jloc) throw ApiError(CPF_E_ARG, "tensor slab size mismatch: expected " + std::to_string(Jloc));
     CPF_CUDA_CHECK(cudaSetDevice(dev));
     if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }  // Y pointer is baked into the graph
@@ -1700,6 +1718,7 @@ struct Engine final : EngineBase {
   }
   // CPTN file -> this rank's slab in device memory, double-buffered through pinned staging
   void load_cptn(const char* path, int64_t payload_off) override {
+    NvtxRange nvtx_("cpf.load_cptn");
     CPF_CUDA_CHECK(cudaSetDevice(dev));
     if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
     const int fd = ::open(path, O_RDONLY);
@@ -1758,6 +1777,7 @@ struct Engine final : EngineBase {
   }
 
   void fit_begin(int variant, double tau, double tol, int max_iters, cpf_status* o) override {
+    NvtxRange nvtx_("cpf.fit_begin (preamble)");
     require_ready();
     if (variant < 0 || variant > 2) throw ApiError(CPF_E_ARG, "unknown variant");
     reset_state(variant, 0.0, tol, max_iters);
@@ -1841,6 +1861,7 @@ struct Engine final : EngineBase {
   static constexpr int kStopMaxIters = 4;
 
   void iteration() {
+    NvtxRange nvtx_("cpf.iteration (eager or captured)");
     const int g = kRunning;
     pdl_now = true;
     mark(0);
@@ -1944,6 +1965,7 @@ struct Engine final : EngineBase {
   }
 
   void fit_step(int n, cpf_status* o) override {
+    NvtxRange nvtx_("cpf.fit_step");
     pull_state();
     const char* env = knob("CPF_NO_GRAPH");
     const bool use_graph = graph_ok && !prof && !(env && env[0] == '1');
@@ -2093,6 +2115,7 @@ struct Engine final : EngineBase {
   // ranks, so rank p forms its block row G[slab_p, :] against every rank's slab (each slab
   // broadcast in turn from its owner) and the block rows are summed across ranks.
   void unfolding_gram(int mode, void* out) override {
+    NvtxRange nvtx_("cpf.unfolding_gram");
     if (!have_tensor) throw ApiError(CPF_E_STATE, "no tensor bound");
     if (mode < 1 || mode > N) throw ApiError(CPF_E_ARG, "mode out of range");
     const int n = mode - 1;
@@ -2183,6 +2206,7 @@ struct Engine final : EngineBase {
   // One ALS (line_search = 0) or ALS-ls step of the bound factors A at iteration t; the history is
   // the iterate before the previous call (none right after set_factors) or set_history's.
   double als_step(int line_search, int t) override {
+    NvtxRange nvtx_("cpf.als_step");
     require_ready();
     als_alloc();
     reset_state(0, 0.0, 0.0, 0);
@@ -2211,6 +2235,7 @@ struct Engine final : EngineBase {
   // on the identity (fdi.cuh).  use_kinv: -1 auto (kernel_is_invertible), 0 K-free, 1 K^{-1}.  Returns a
   // CPF_ERR_* code (0 = ok).  Needs factors only (no tensor).
   int fast_damped_inverse(double mu, int use_kinv, void* gt_out, void* d_out) override {
+    NvtxRange nvtx_("cpf.fast_damped_inverse");
     if (!have_factors) throw ApiError(CPF_E_STATE, "no factors bound");
     if (!(mu > 0.0)) throw ApiError(CPF_E_ARG, "mu must be positive");
     if (N < 2) throw ApiError(CPF_E_ARG, "kernel inverse needs at least two modes");

@@ -21,7 +21,7 @@ eng.set_tensor_device(y.data_ptr(), y.numel())
 eng.set_factors(np.concatenate([f.reshape(-1, order="F") for f in synth.init_factors(cfg, 0)]))
 eng.fit_begin("auto", synth.tau_for_unit_mu(cfg, 0), 0.0, 5)
 eng.fit_step(5)
-buf = (ctypes.c_longlong * 16)()
+buf = (ctypes.c_longlong * 24)()
 lib.cpf_debug_panel_cycles(buf)
 c = np.array(buf[:], dtype=np.float64)
 npanels = c[7]
