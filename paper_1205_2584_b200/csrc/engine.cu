@@ -227,6 +227,11 @@ struct Engine final : EngineBase {
   T* invL = nullptr;    // 2 slots (double-buffered across look-ahead steps)
   int* gring = nullptr; // 2 gather lists + counts
   cudaStream_t s2 = nullptr;
+  // progressive triangular inverse (tri_progress): side stream of the look-ahead LU + its events
+  cudaStream_t s4 = nullptr, sS4 = nullptr;
+  cudaEvent_t evT = nullptr, evT2 = nullptr;
+  bool tri_prog = true;
+  bool tri_in_lu = false;  // the last lu_factor already produced PhiInv
   cudaEvent_t evP = nullptr, evB = nullptr, evJ = nullptr;
   cudaEvent_t evB2[2] = {nullptr, nullptr};
   size_t lu_smem = 0;
@@ -348,6 +353,10 @@ struct Engine final : EngineBase {
     for (auto e : evB2) if (e) cudaEventDestroy(e);
     if (evJ) cudaEventDestroy(evJ);
     if (s2) cudaStreamDestroy(s2);
+    if (evT) cudaEventDestroy(evT);
+    if (evT2) cudaEventDestroy(evT2);
+    if (s4) cudaStreamDestroy(s4);
+    if (sS4) cudaStreamDestroy(sS4);
     if (evF) cudaEventDestroy(evF);
     if (evS0) cudaEventDestroy(evS0);
     if (evS1) cudaEventDestroy(evS1);
@@ -482,6 +491,8 @@ struct Engine final : EngineBase {
   // SMs left to the LU while pass B runs alongside it (CPF_LU_RESERVE overrides)
   // (HBM-bound Ozaki pass B: 40, measured best of 24..48 at config 4; DMMA pass B: 24)
   int kLuReserveSms = 24;
+  int kSpecReserveSms = 20;  // SMs pass A leaves to a speculated core system (plan_spec)
+  bool spec_a_side = true;   // pass A beside the speculated core system runs on the low-priority stream
   // pass B overlapped with the LU runs as a persistent grid on nsm - kLuReserveSms SMs, so the LU's
   // small panel clusters and GEMM updates always find free SMs (CPF_PERSISTENT_B=0: plain grid)
   const bool persistent_b = [] { const char* e = knob("CPF_PERSISTENT_B"); return !(e && e[0] == '0'); }();
@@ -630,7 +641,16 @@ struct Engine final : EngineBase {
       int plo = 0, phi = 0;
       CPF_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&plo, &phi));
       CPF_CUDA_CHECK(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, phi));
+      // one level below the panels / trailing updates: the merges fill SMs the LU leaves idle and
+      // must not hold up a panel cluster's launch
+      int ptri = std::min(plo, phi + 1);
+      if (const char* e = knob("CPF_TRI_PRIO")) ptri = std::max(phi, std::min(plo, phi + atoi(e)));
+      CPF_CUDA_CHECK(cudaStreamCreateWithPriority(&s4, cudaStreamNonBlocking, ptri));
+      CPF_CUDA_CHECK(cudaStreamCreateWithPriority(&sS4, cudaStreamNonBlocking, ptri));
     }
+    CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evT, cudaEventDisableTiming));
+    CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evT2, cudaEventDisableTiming));
+    if (const char* e = knob("CPF_TRI_PROG")) tri_prog = e[0] != '0';
     CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evP, cudaEventDisableTiming));
     CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
     CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evJ, cudaEventDisableTiming));
@@ -779,14 +799,17 @@ struct Engine final : EngineBase {
       use_oz = true;
     }
   }
-  // speculative rejection branch: on where the tensor passes are short next to the LU (FMA-pass
-  // tensors: C2 416 -> 446, C3 693 -> 732 it/s); off for the long int8 / DMMA passes (config 4:
-  // pass A on 108 SMs beside the branch's LU, 2.3 -> 2.7 ms, costs more on the ~75 % accepted
-  // steps than the skipped LU saves: 157.7 -> 151.7 it/s).  CPF_SPEC=0/1 overrides.
+  // speculative rejection branch: on for the FMA-pass tensors (C2 416 -> 446, C3 693 -> 732 it/s)
+  // and, since pass A runs on the low-priority stream beside it (spec_a_side), for the int8 passes
+  // (config 4: 172.6 -> 183 it/s; with pass A on the LU's own priority level the branch's trailing
+  // updates were held back until the pass's persistent grid retired and the branch lost).  Off
+  // for the fp64 DMMA passes (not measured with the side stream).  CPF_SPEC=0/1 overrides.
   void plan_spec() {
-    use_spec = use_inv && lu3_rpt && !use_oz && !use_dmma;
+    use_spec = use_inv && lu3_rpt && (use_oz || !use_dmma);
     if (const char* e = knob("CPF_SPEC")) use_spec = e[0] == '1' && use_inv && lu3_rpt;
     if (!use_spec) return;
+    if (const char* e = knob("CPF_SPEC_RESERVE")) kSpecReserveSms = atoi(e);
+    if (const char* e = knob("CPF_SPEC_A_SIDE")) spec_a_side = e[0] != '0';
     const size_t R2 = (size_t)R * R;
     PhiS = dalloc<T>((size_t)nB * nB);
     PhiInvS = dalloc<T>((size_t)nB * nB);
@@ -806,6 +829,7 @@ struct Engine final : EngineBase {
     luS.ticket = luS.info + 1;
     luS.ready = luS.ticket + 4;
     spec_sing = dalloc<int>(2);
+    luS.latch = dalloc<int>((nB + kLuMaxKB - 1) / kLuMaxKB + 2);
     if (lp_cfg) {
       alloc_lp(lpS);
       lpS.perm = luS.perm;
@@ -832,6 +856,7 @@ struct Engine final : EngineBase {
     std::swap(lp, lpS);
     std::swap(s, sS);
     std::swap(s2, sS2);
+    std::swap(s4, sS4);
   }
 
   // one-time digit-plane images of the bound tensor (both passes), stream-ordered after the upload.
@@ -859,6 +884,7 @@ struct Engine final : EngineBase {
         ozYA = ozYB = nullptr;
         kLuReserveSms = 24;
         if (const char* e = knob("CPF_LU_RESERVE")) kLuReserveSms = atoi(e);
+        if (use_dmma && !knob("CPF_SPEC")) use_spec = false;  // fp64 DMMA passes: branch off (plan_spec)
         return;
       }
       k_oz_split_y<0><<<nsm_ * 16, 256, 0, s>>>(Yd, oa, ozFrowA, ozYA);
@@ -1109,10 +1135,24 @@ struct Engine final : EngineBase {
         launch(k_oz_split_b, dim3(R), 256, 0, (const double*)WNc, Cloc, R, RP, ozBA, ozFr, oz_bad_ptr(0), cst, cfl,
                gate);
         // beside a speculated core system, pass A leaves the LU its SMs like pass B does
-        const int nch = std::max(1, (use_spec ? nsm_ - kLuReserveSms : nsm_) / oa.nb);
+        const int nch = std::max(1, (use_spec ? nsm_ - kSpecReserveSms : nsm_) / oa.nb);
         const OzOut oo{(const double*)A1c, (const double*)KMc, RP, nch, (Lmid + nch - 1) / nch, ozM1, ozZ};
+        // beside a speculated core system the pass runs on the low-priority stream (like pass B in
+        // the fork): on the LU's own priority level its resident persistent grid held back the
+        // branch's trailing updates until it retired
+        const bool side = use_spec && spec_a_side && ls == s && gate == kRunning;
+        if (side) {
+          CPF_CUDA_CHECK(cudaEventRecord(evF, s));
+          CPF_CUDA_CHECK(cudaStreamWaitEvent(s3, evF, 0));
+          ls = s3;
+        }
         launch(k_oz_pass<0>, dim3((unsigned)(oa.nb * nch)), kOzThreads, kOzSmem, (const uint8_t*)ozYA,
                (const int*)ozFrowA, (const uint8_t*)ozBA, (const int*)ozFr, oa, oo, cst, cfl, go);
+        if (side) {
+          ls = s;
+          CPF_CUDA_CHECK(cudaEventRecord(evG, s3));
+          CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evG, 0));
+        }
         ph_end();
         launch(k_m1_reduce<T>, nblocks(I1 * R, 32), 256, 0, (const T*)ozM1, nch, I1, R, RP, pa_out, cst, cfl, go);
         launch(k_z_reduce<T>, nblocks(Lmid * R, 256), 256, 0, (const T*)ozZ, oa.nb, Lmid, R, RP, pa_out + I1 * R,
@@ -1389,9 +1429,10 @@ struct Engine final : EngineBase {
     CPF_CUDA_CHECK(cudaGetLastError());
   }
 
-  void lu_factor(int gate_running) {
+  void lu_factor(int gate_running, bool with_inverse = false) {
     NvtxRange nvtx_("cpf.lu");
     ph_begin(kPhLU);
+    tri_in_lu = false;
     if (lp_cfg) {
       lu_factor_lp(gate_running);
       if (!spec_capture) launch(k_lu_info_to_err, 1, 1, 0, (const int*)lu.info, st);
@@ -1409,6 +1450,7 @@ struct Engine final : EngineBase {
       // and last read the slot panel k overwrites).
       const int KB = kLuMaxKB;
       const int np = (nB + KB - 1) / KB;
+      if (lu.latch) CPF_CUDA_CHECK(cudaMemsetAsync(lu.latch, 0, sizeof(int), s));
       CPF_CUDA_CHECK(cudaEventRecord(evJ, s));
       CPF_CUDA_CHECK(cudaStreamWaitEvent(s2, evJ, 0));
       for (int k = 0; k < np; ++k) {
@@ -1447,8 +1489,19 @@ struct Engine final : EngineBase {
         lu_update_cols(k0, kb, nb1, nB, invl, s2, gate_running);
         CPF_CUDA_CHECK(cudaEventRecord(evB2[slot], s2));
         CPF_CUDA_CHECK(cudaEventRecord(evB, s2));
+        if (with_inverse && tri_prog) {
+          // s2's step k finalised the leading 32 (k + 1) rows/columns of L and U: the merges of the
+          // triangular inverse that live inside it run on s4, beside the remaining panels
+          CPF_CUDA_CHECK(cudaStreamWaitEvent(s4, evB, 0));
+          tri_progress(k, np, gate_running);
+        }
       }
       CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evB, 0));
+      if (with_inverse && tri_prog) {
+        CPF_CUDA_CHECK(cudaEventRecord(evT2, s4));
+        CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evT2, 0));
+        tri_in_lu = true;
+      }
       if (!spec_capture) launch(k_lu_info_to_err, 1, 1, 0, (const int*)lu.info, st);
       ph_end();
       return;
@@ -1504,26 +1557,60 @@ struct Engine final : EngineBase {
   static constexpr int kTriSplit = 4;
   T* TriPart = nullptr;   // split-K partials: kTriSplit x nB x nB
   T* TriPartS = nullptr;  // the speculative branch's
+  // Progressive form of tri_invert: after the LU's step k (0-based 32-column block k, np blocks)
+  // the blocks 0..k of L and U are final.  Launch on s4 the diagonal inverse of block k and, level
+  // by level, every merge whose pair ends at block k (the last block closes the ragged pairs).
+  // Same kernels, same operation order per output element as the batched launches -> bitwise
+  // identical inverse; only the tail (the pairs that end at the last block) stays behind the LU.
+  void tri_progress(int k, int np, int gate_running) {
+    const LmDeviceState* cst = st;
+    k_tri_inv_diag<T><<<1, 64, 0, s4>>>((const T*)Phi, nB, PhiInv, cst, gate_running, k, k);
+    ++nlaunch;
+    const bool last = k == np - 1;
+    for (int sz = 32; sz < nB; sz *= 2) {
+      const int w = sz / 32;  // blocks per half
+      if (!last && (k + 1) % (2 * w) != 0) break;  // higher levels end at the same block or later
+      const int pair = k / (2 * w);
+      if ((2 * pair + 1) * sz >= nB) continue;  // single (ragged) half: nothing to merge
+      const int ks = tri_split(sz);
+      const dim3 grid((sz + 63) / 64, (sz + 63) / 64, 2 * ks);
+      const dim3 rgrid(std::max(1, std::min(256, (int)nblocks((int64_t)sz * sz, 256))), 2);
+      T* part = ks > 1 ? TriPart : (T*)nullptr;
+      k_tri_level<T, 0><<<grid, 256, 0, s4>>>((const T*)Phi, PhiInv, TriTmp, nB, sz, cst, gate_running, ks, part, pair, k);
+      ++nlaunch;
+      if (ks > 1) {
+        k_tri_reduce<T, 0><<<rgrid, 256, 0, s4>>>(PhiInv, TriTmp, (const T*)TriPart, ks, nB, sz, cst, gate_running, pair, k);
+        ++nlaunch;
+      }
+      k_tri_level<T, 1><<<grid, 256, 0, s4>>>((const T*)Phi, PhiInv, TriTmp, nB, sz, cst, gate_running, ks, part, pair, k);
+      ++nlaunch;
+      if (ks > 1) {
+        k_tri_reduce<T, 1><<<rgrid, 256, 0, s4>>>(PhiInv, TriTmp, (const T*)TriPart, ks, nB, sz, cst, gate_running, pair, k);
+        ++nlaunch;
+      }
+    }
+    CPF_CUDA_CHECK(cudaGetLastError());
+  }
   void tri_invert(int gate_running) {
     NvtxRange nvtx_("cpf.tri_inverse");
     ph_begin(kPhLU);
     const int nblk = (nB + 31) / 32;
-    launch(k_tri_inv_diag<T>, nblk, 64, 0, (const T*)Phi, nB, PhiInv, (const LmDeviceState*)st, gate_running);
+    launch(k_tri_inv_diag<T>, nblk, 64, 0, (const T*)Phi, nB, PhiInv, (const LmDeviceState*)st, gate_running, 0, 200);
     for (int sz = 32; sz < nB; sz *= 2) {
       const int npairs = (nB + 2 * sz - 1) / (2 * sz);
       const int ks = tri_split(sz);
       const dim3 grid((sz + 63) / 64, (sz + 63) / 64, 2 * npairs * ks);
       const dim3 rgrid(std::max(1, std::min(256, (int)nblocks((int64_t)sz * sz, 256))), 2 * npairs);
       launch(k_tri_level<T, 0>, grid, 256, 0, (const T*)Phi, PhiInv, TriTmp, nB, sz, (const LmDeviceState*)st,
-             gate_running, ks, ks > 1 ? TriPart : (T*)nullptr);
+             gate_running, ks, ks > 1 ? TriPart : (T*)nullptr, 0, 200);
       if (ks > 1)
         launch(k_tri_reduce<T, 0>, rgrid, 256, 0, PhiInv, TriTmp, (const T*)TriPart, ks, nB, sz, (const LmDeviceState*)st,
-               gate_running);
+               gate_running, 0, 200);
       launch(k_tri_level<T, 1>, grid, 256, 0, (const T*)Phi, PhiInv, TriTmp, nB, sz, (const LmDeviceState*)st,
-             gate_running, ks, ks > 1 ? TriPart : (T*)nullptr);
+             gate_running, ks, ks > 1 ? TriPart : (T*)nullptr, 0, 200);
       if (ks > 1)
         launch(k_tri_reduce<T, 1>, rgrid, 256, 0, PhiInv, TriTmp, (const T*)TriPart, ks, nB, sz, (const LmDeviceState*)st,
-               gate_running);
+               gate_running, 0, 200);
     }
     ph_end();
   }
@@ -1582,9 +1669,9 @@ struct Engine final : EngineBase {
            (const T*)Gp, (const T*)Gf, (const LmDeviceState*)st, gr);
     if (test_singular) launch(k_test_zero_col<T>, 1, 256, 0, Phi, nB, (const LmDeviceState*)st, mode == 1 ? 2 : 1);
     mark(5);
-    lu_factor(gr);
+    lu_factor(gr, use_inv);
     mark(6);
-    if (use_inv) tri_invert(gr);
+    if (use_inv && !tri_in_lu) tri_invert(gr);
     mark(7);
   }
 

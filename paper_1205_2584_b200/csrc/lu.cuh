@@ -38,7 +38,26 @@ struct LuWork {
   int* info;       // 1: first zero pivot (1-based), 0 = none
   int* ticket;     // 2 counters for the substitution kernels
   int* ready;      // ceil(n/32) flags
+  int* latch = nullptr;  // speculative branch only: per-panel abandonment latch (panel_gated)
 };
+
+// Gate of the cluster panel kernels.  Their CTAs synchronise with each other, so all of them must
+// take the same branch; the speculative branch (gate 3) may nevertheless be abandoned between two
+// panels: panel k latches the decision for panel k + 1 (one thread, at its end; the stream order
+// makes it visible and stable for every CTA of the next panel), an abandoned panel passes it on.
+__device__ __forceinline__ bool panel_gated(const LmDeviceState* st, int gate_running, const LuWork& w, int k) {
+  if (gate_running != 3 || !w.latch) return lu_gated_sync(st, gate_running);
+  if (lu_gated(st, 1)) return true;
+  if (w.latch[k]) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) w.latch[k + 1] = 1;
+    return true;
+  }
+  return false;
+}
+__device__ __forceinline__ void panel_latch_next(const LmDeviceState* st, int gate_running, const LuWork& w, int k) {
+  if (gate_running == 3 && w.latch && blockIdx.x == 0 && threadIdx.x == 0)
+    w.latch[k + 1] = ld_volatile_int(&st->accept_iter) == st->spec_iter + 1 ? 1 : 0;
+}
 
 __global__ void k_lu_init(int* perm, int n, int* info) {
   pdl_wait();

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
                                                        PanelPrev<T> pv) {
   pdl_wait();
   static_assert(KB == kLuMaxKB, "panel width");
-  if (lu_gated_sync(st, gate_running)) return;
+  if (panel_gated(st, gate_running, w, k0 / KB)) return;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
     }
   }
   cluster.sync();
+  panel_latch_next(st, gate_running, w, k0 / KB);
 }
 
 // U12 = inv(L11) A12 in place: CTA per 64-column tile of A12 (rows k0..k0+kb).

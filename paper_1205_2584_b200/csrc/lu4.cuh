@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
                                                        T* __restrict__ invL, const LmDeviceState* st, int gate_running,
                                                        PanelPrev<T> pv) {
   pdl_wait();
-  if (lu_gated_sync(st, gate_running)) return;
+  if (panel_gated(st, gate_running, w, k0 / kLuMaxKB)) return;
   lu_trace(0, k0 / kLuMaxKB, 0);
 #ifdef CPF_PANEL_TIMING
   const long long seg0 = clock64();
@@ -373,6 +373,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu4(T* __restrict__ A, int n,
   if (rank == 0 && tid == 0) atomicAdd((unsigned long long*)&g_panel_seg[3], (unsigned long long)(clock64() - seg0));
 #endif
   lu_trace(0, k0 / kLuMaxKB, 1);
+  panel_latch_next(st, gate_running, w, k0 / kLuMaxKB);
 }
 
 }  // namespace cpf

@@ -6,7 +6,9 @@
 //
 // Storage: Inv (n x n, column-major) holds inv(L) strictly below the diagonal (unit diagonal
 // implicit) and inv(U) on and above it -- the same packing as the LU factors.
-// Algorithm (recursive doubling, every level one batched launch per product):
+// Algorithm (recursive doubling; batched: every level one launch per product; progressive: each
+// merge launched on a side stream as soon as the LU has finalised its leading block, blk0 / pair0
+// select the block / pair -- engine.cu tri_progress):
 //   level 0: invert every 32x32 diagonal block (one CTA each);
 //   level s: for adjacent blocks (b1, b2) of size s
 //     L: inv([L11 0; L21 L22])  -> X21 = -inv(L22) (L21 inv(L11))
@@ -20,11 +22,12 @@ namespace cpf {
 
 template <class T>
 __global__ void __launch_bounds__(64) k_tri_inv_diag(const T* __restrict__ LU, int n, T* __restrict__ Inv,
-                                                     const LmDeviceState* st, int gate_running) {
+                                                     const LmDeviceState* st, int gate_running, int blk0, int tstep) {
   pdl_wait();
   if (lu_gated(st, gate_running)) return;
+  lu_trace(1, 256 + tstep, 0);
   __shared__ T blk[32][33];
-  const int b0 = blockIdx.x * 32;
+  const int b0 = (blk0 + blockIdx.x) * 32;
   const int bs = min(32, n - b0);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int e = tid; e < 32 * 32; e += 64) {
@@ -33,7 +36,7 @@ __global__ void __launch_bounds__(64) k_tri_inv_diag(const T* __restrict__ LU, i
   }
   __syncthreads();
   const int c = lane;
-  if (c >= bs) return;
+  if (c >= bs) { lu_trace(1, 256 + tstep, 1); return; }
   T x[32];
   if (wid == 0) {
     // unit lower: x = inv(L) e_c, rows i > c
@@ -60,6 +63,7 @@ __global__ void __launch_bounds__(64) k_tri_inv_diag(const T* __restrict__ LU, i
     for (int i = 0; i < 32; ++i)
       if (i <= c) Inv[(int64_t)(b0 + i) + (int64_t)n * (b0 + c)] = x[i];
   }
+  lu_trace(1, 256 + tstep, 1);
 }
 
 // Operand kinds of the level products
@@ -88,11 +92,11 @@ __device__ __forceinline__ T tri_elem(const T* M, int n, int r, int c, int kind)
 template <class T, int STEP>
 __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* __restrict__ Inv, T* __restrict__ Tmp,
                                                    int n, int s, const LmDeviceState* st, int gate_running,
-                                                   int ksplit = 1, T* __restrict__ part = nullptr) {
+                                                   int ksplit, T* __restrict__ part, int pair0, int tstep) {
   pdl_wait();
   if (lu_gated(st, gate_running)) return;
   const int ks = blockIdx.z % ksplit, pt = blockIdx.z / ksplit;
-  const int pair = pt >> 1, tri = pt & 1;
+  const int pair = pair0 + (pt >> 1), tri = pt & 1;
   const int b1 = 2 * pair * s, b2 = b1 + s;
   if (b2 >= n) return;
   const int s1 = s, s2 = min(s, n - b2);
@@ -114,6 +118,7 @@ __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* 
   }
   const int tm = blockIdx.x * 64, tn = blockIdx.y * 64;
   if (tm >= m || tn >= nn) return;
+  lu_trace(1, 256 + tstep, 0);
   constexpr int KS = 16 * 8 / (int)sizeof(T);  // K rows per stage (8 for complex: 48 KB static smem)
   // triangular operands: skip the K range that only multiplies zeros
   int kbeg = 0, kend = kk;
@@ -209,6 +214,7 @@ __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* 
           const int r = tm + wm + 8 * i + g, c = tn + wn + 8 * j + 2 * t4 + h;
           if (r < m && c < nn) Cm[(int64_t)(rc + r) + (int64_t)n * (cc + c)] = alpha * dacc[i][j][h];
         }
+    lu_trace(1, 256 + tstep, 1);
     return;
   } else {
     for (int k0 = kbeg; k0 < kend; k0 += KS) {
@@ -237,6 +243,7 @@ __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* 
         const int r = tm + tx + 16 * i, c = tn + ty + 16 * j;
         if (r < m && c < nn) Cm[(int64_t)(rc + r) + (int64_t)n * (cc + c)] = scale(acc[i][j], alpha);
       }
+    lu_trace(1, 256 + tstep, 1);
   }
 }
 
@@ -244,10 +251,10 @@ __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* 
 // STEP 1 -> Inv.  grid.y = 2 * npairs (pair, triangle).
 template <class T, int STEP>
 __global__ void k_tri_reduce(T* __restrict__ Inv, T* __restrict__ Tmp, const T* __restrict__ part, int ksplit, int n,
-                             int s, const LmDeviceState* st, int gate_running) {
+                             int s, const LmDeviceState* st, int gate_running, int pair0, int tstep) {
   pdl_wait();
   if (lu_gated(st, gate_running)) return;
-  const int pair = blockIdx.y >> 1, tri = blockIdx.y & 1;
+  const int pair = pair0 + (blockIdx.y >> 1), tri = blockIdx.y & 1;
   const int b1 = 2 * pair * s, b2 = b1 + s;
   if (b2 >= n) return;
   const int s1 = s, s2 = min(s, n - b2);
@@ -262,6 +269,7 @@ __global__ void k_tri_reduce(T* __restrict__ Inv, T* __restrict__ Tmp, const T* 
     for (int k = 1; k < ksplit; ++k) v = add(v, part[(size_t)k * nn2 + off]);
     dst[off] = v;
   }
+  lu_trace(1, 256 + tstep, 1);
 }
 
 // y = op(Inv) x for the packed triangular inverse: LOWER -> unit-lower inv(L), else inv(U).

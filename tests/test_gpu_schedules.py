@@ -4,7 +4,8 @@ bitwise deterministic by construction (fixed-order reductions, no atomics on dat
 of scheduling the same fit must give BITWISE identical traces and factors:
   graph replay (default) | eager launches (CPF_NO_GRAPH=1) | serial fork, no pass-B / LU overlap
   (CPF_SERIAL=1) | no programmatic dependent launch (CPF_PDL=0) | speculative rejection branch
-  on / off (CPF_SPEC) | repeated runs.
+  on / off (CPF_SPEC) | batched instead of progressive triangular inverse (CPF_TRI_PROG=0) |
+  repeated runs.
 A missing stream / event dependency, an mbarrier or flag race in the LU panels or the tensor-pass
 pipelines would show up as a difference under one of these schedules."""
 
@@ -20,6 +21,8 @@ SCHEDULES = [
     {"CPF_PDL": "0"},
     {"CPF_SPEC": "1"},
     {"CPF_SPEC": "0"},
+    {"CPF_TRI_PROG": "0"},
+    {"CPF_TRI_PROG": "0", "CPF_SPEC": "1"},
     {"CPF_NO_GRAPH": "1", "CPF_SERIAL": "1", "CPF_PDL": "0"},
 ]
 
