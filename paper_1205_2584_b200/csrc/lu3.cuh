@@ -131,8 +131,12 @@ __device__ __forceinline__ void panel_load(T (&a)[RPT][kLuMaxKB], const T* __res
 #ifdef CPF_PANEL_TIMING
   long long pt0 = clock64();
 #endif
+  // Global round trips are what a panel pays for under a saturated memory system (the pass that
+  // runs beside the LU): the gather list is read whole (it does not wait for its count), and this
+  // thread's own rows plus the first L21 chunk are requested right after the A12 rows, so they fly
+  // during the U12 product; the remaining L21 chunks are prefetched one chunk ahead.
   const int G = *pv.gcount;
-  for (int e = tid; e < 2 * G; e += NTHR) gl[e] = pv.gather[e];
+  for (int e = tid; e < 4 * KB; e += NTHR) gl[e] = pv.gather[e];
   if (linv)
     for (int e = tid; e < KB * KB; e += NTHR) linv[e] = pv.invL[e];
   __syncthreads();
@@ -145,22 +149,45 @@ __device__ __forceinline__ void panel_load(T (&a)[RPT][kLuMaxKB], const T* __res
   // A12 (the step's top rows of this block, interchanged) -> u12[i][q]; NTHR % KB == 0, so a
   // thread's elements share one row i and one gather lookup
   static_assert(NTHR % KB == 0, "panel threads");
+  constexpr int NA = (KB * KB + NTHR - 1) / NTHR;
+  T a12[NA];
   {
     const int i = tid % KB;
     const int64_t srow = i < pv.kbp ? src_of(pv.kp0 + i) : 0;
-    for (int e = tid; e < KB * KB; e += NTHR) {
+#pragma unroll
+    for (int t = 0; t < NA; ++t) {
+      const int e = tid + t * NTHR;
       const int q = e / KB;
-      T v = zero_of<T>();
-      if (i < pv.kbp && q < kb) v = A[srow + (int64_t)lda * (k0 + q)];
-      u12[i * KB + q] = v;
+      a12[t] = (e < KB * KB && i < pv.kbp && q < kb) ? A[srow + (int64_t)lda * (k0 + q)] : zero_of<T>();
     }
+  }
+  // this panel's rows (interchanged block row) and the first L21 chunk: in flight during U12
+  T v[RPT][KB];
+  const T* lrow[RPT];
+  T l[RPT][8];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int r = k0 + myrow[j];
+    const T* src = A + (int64_t)(alive[j] ? src_of(r) : 0) + (int64_t)lda * k0;
+#pragma unroll
+    for (int q = 0; q < KB; ++q) v[j][q] = (alive[j] && q < kb) ? src[(int64_t)lda * q] : zero_of<T>();
+    lrow[j] = A + (int64_t)(alive[j] ? r : 0) + (int64_t)lda * pv.kp0;
+  }
+#pragma unroll
+  for (int j = 0; j < RPT; ++j)
+#pragma unroll
+    for (int p = 0; p < 8; ++p) l[j][p] = (alive[j] && p < pv.kbp) ? lrow[j][(int64_t)lda * p] : zero_of<T>();
+#pragma unroll
+  for (int t = 0; t < NA; ++t) {
+    const int e = tid + t * NTHR;
+    if (e < KB * KB) u12[(tid % KB) * KB + e / KB] = a12[t];
   }
   __syncthreads();
   PSEG(4, pt0);
   // U12 = inv(L11) A12 (same summation order as k_u12)
-  T uv[(KB * KB + NTHR - 1) / NTHR];
+  T uv[NA];
 #pragma unroll
-  for (int t = 0; t < (KB * KB + NTHR - 1) / NTHR; ++t) {
+  for (int t = 0; t < NA; ++t) {
     const int e = tid + t * NTHR;
     T acc = zero_of<T>();
     if (e < KB * KB) {
@@ -177,34 +204,25 @@ __device__ __forceinline__ void panel_load(T (&a)[RPT][kLuMaxKB], const T* __res
   }
   __syncthreads();
 #pragma unroll
-  for (int t = 0; t < (KB * KB + NTHR - 1) / NTHR; ++t) {
+  for (int t = 0; t < NA; ++t) {
     const int e = tid + t * NTHR;
     if (e < KB * KB) u12[e] = uv[t];
   }
   __syncthreads();
   PSEG(5, pt0);
-  // this panel's rows: interchanged block row minus L21 U12.  With a stage (the caller's
-  // per-thread smem slots, stride RPT*NTHR) the frame is loaded afterwards, so the update does not
-  // add to the column loop's register pressure.  All RPT rows are updated together: each U12 value
-  // read from shared memory serves every row of the thread.
+  // rows minus L21 U12.  With a stage (the caller's per-thread smem slots, stride RPT*NTHR) the
+  // frame is loaded afterwards, so the update does not add to the column loop's register
+  // pressure.  All RPT rows are updated together: each U12 value read from shared memory serves
+  // every row of the thread.
   {
-    T v[RPT][KB];
-    const T* lrow[RPT];
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-      const int r = k0 + myrow[j];
-      const T* src = A + (int64_t)(alive[j] ? src_of(r) : 0) + (int64_t)lda * k0;
-#pragma unroll
-      for (int q = 0; q < KB; ++q) v[j][q] = (alive[j] && q < kb) ? src[(int64_t)lda * q] : zero_of<T>();
-      lrow[j] = A + (int64_t)(alive[j] ? r : 0) + (int64_t)lda * pv.kp0;
-    }
 #pragma unroll 1
     for (int p0 = 0; p0 < pv.kbp; p0 += 8) {
-      T l[RPT][8];
+      T ln[RPT][8];  // next chunk, requested before this chunk's products
 #pragma unroll
       for (int j = 0; j < RPT; ++j)
 #pragma unroll
-        for (int p = 0; p < 8; ++p) l[j][p] = (alive[j] && p0 + p < pv.kbp) ? lrow[j][(int64_t)lda * (p0 + p)] : zero_of<T>();
+        for (int p = 0; p < 8; ++p)
+          ln[j][p] = (alive[j] && p0 + 8 + p < pv.kbp) ? lrow[j][(int64_t)lda * (p0 + 8 + p)] : zero_of<T>();
 #pragma unroll
       for (int p = 0; p < 8; ++p) {
         const T* ur = u12 + (p0 + p) * KB;
@@ -215,6 +233,10 @@ __device__ __forceinline__ void panel_load(T (&a)[RPT][kLuMaxKB], const T* __res
           for (int j = 0; j < RPT; ++j) fms_acc(v[j][q], l[j][p], u);
         }
       }
+#pragma unroll
+      for (int j = 0; j < RPT; ++j)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) l[j][p] = ln[j][p];
     }
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
