@@ -179,6 +179,10 @@ int cpf_pinv_psd(int device, int kind, int R, const void* gram, void* out);
  * Phases: 0 pass A, 1 pass B, 2 LU factor, 3 solves, 4 other; counts = launches per phase. */
 int cpf_engine_profile(cpf_engine* e, int enable);
 int cpf_engine_phase_times(cpf_engine* e, double* ms_out, int64_t* counts_out, int nphases);
+/* Longest single instance of each phase since profiling was last switched on (after a
+ * cpf_engine_phase_times call): a complete factorisation / pass, where the per-phase totals also
+ * hold instances whose kernels were gated off (rejected step, abandoned speculative branch). */
+int cpf_engine_phase_max(cpf_engine* e, double* ms_out, int nphases);
 /* G_n = Y_(n) Y_(n)^H (I_n x I_n, column-major) of the bound tensor, for the SVD initialisation
  * (kruskal.py:227-242).  Sharded tensors: every mode (mode N by broadcasting each slab in turn;
  * every rank returns the full matrix). */

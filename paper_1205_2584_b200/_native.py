@@ -92,6 +92,7 @@ EXPORTED_SYMBOLS = (
     "cpf_engine_flm_step",
     "cpf_engine_profile",
     "cpf_engine_phase_times",
+    "cpf_engine_phase_max",
     "cpf_engine_launch_count",
     "cpf_engine_unfolding_gram",
     "cpf_engine_pass_impl",
@@ -142,6 +143,7 @@ def _declare(lib) -> None:
         "cpf_engine_flm_step": (I, [P, D, I, I, P, ctypes.POINTER(I)]),
         "cpf_engine_profile": (I, [P, I]),
         "cpf_engine_phase_times": (I, [P, ctypes.POINTER(D), ctypes.POINTER(I64), I]),
+        "cpf_engine_phase_max": (I, [P, ctypes.POINTER(D), I]),
         "cpf_engine_launch_count": (I64, [P]),
         "cpf_engine_unfolding_gram": (I, [P, I, P]),
         "cpf_engine_pass_impl": (I, [P]),
@@ -418,6 +420,11 @@ class Engine:
         cnt = (ctypes.c_int64 * n)()
         self._check(self._lib.cpf_engine_phase_times(self._h, ms, cnt, n))
         return list(ms), list(cnt)
+
+    def phase_max(self, n: int = 5):
+        ms = (ctypes.c_double * n)()
+        self._check(self._lib.cpf_engine_phase_max(self._h, ms, n))
+        return list(ms)
 
     def unfolding_gram(self, mode: int) -> np.ndarray:
         d = self.dims[mode - 1]  # sharded mode N: every rank receives the full I_N x I_N Gram

@@ -129,6 +129,7 @@ struct EngineBase {
   virtual int flm_step(double mu, int variant, int refine, void* out) = 0;
   virtual void profile(int on) = 0;
   virtual void phase_times(double* ms, int64_t* cnt, int n) = 0;
+  virtual void phase_max(double* ms, int n) = 0;
   virtual int64_t launches() const = 0;
   virtual int pass_impl() const = 0;
   virtual void pass_guard(int64_t* fallbacks, int* rejected) = 0;
@@ -172,6 +173,9 @@ struct Engine final : EngineBase {
   // explicit (factored) inverse of Phi: B w = inv(U) inv(L) P w as two triangular mat-vecs
   T *PhiInv = nullptr, *TriTmp = nullptr, *yvec = nullptr, *tmv_part = nullptr;
   bool use_inv = false;
+  bool use_blkinv = false;            // !use_inv: substitution over inverted diagonal blocks
+  int blk_db = 1024;                  // its diagonal block size (power of two >= 64)
+  int tri_cap() const { return use_inv ? nB : std::min(nB, blk_db); }  // merge levels stay below this
   T *A1c = nullptr, *KMc = nullptr, *WNc = nullptr, *zpart = nullptr, *m1part = nullptr, *bpart = nullptr;
   T *A1r = nullptr, *KMr = nullptr, *WNr = nullptr;  // non-conj operands of the direct residual
   T *pa_out = nullptr, *pb_out = nullptr, *pb_all = nullptr;
@@ -271,6 +275,7 @@ struct Engine final : EngineBase {
   std::vector<Ev> evs;
   double ph_ms[kNumPhases] = {0};
   int64_t ph_cnt[kNumPhases] = {0};
+  double ph_max[kNumPhases] = {0};  // longest single instance since profiling was switched on
 
   // ------------------------------------------------------------------------------------------
   Engine(int device, int order, const int64_t* d, int rank, int wr, int ws, const void* uid,
@@ -457,6 +462,21 @@ struct Engine final : EngineBase {
       if (nB > 256) TriPart = dalloc<T>((size_t)kTriSplit * nB * nB);
       yvec = dalloc<T>(nB);
       tmv_part = dalloc<T>((size_t)((nB + kTmvCols - 1) / kTmvCols) * nB);
+    } else {
+      // block-inverse substitution (tri_inv.cuh): inverted blk_db x blk_db diagonal blocks
+      use_blkinv = true;
+      if (const char* e = knob("CPF_BLK_INV")) use_blkinv = e[0] != '0';
+      if (const char* e = knob("CPF_BLK_DB")) {
+        int v = 64;
+        while (v < atoi(e)) v *= 2;
+        blk_db = v;
+      }
+      if (use_blkinv) {
+        PhiInv = dalloc<T>((size_t)nB * nB);
+        TriTmp = dalloc<T>((size_t)nB * nB);
+        TriPart = dalloc<T>((size_t)kTriSplit * nB * nB);
+        tmv_part = dalloc<T>((size_t)((nB + kTmvCols - 1) / kTmvCols) * nB);
+      }
     }
     A1c = dalloc<T>((size_t)I1 * RP + 2);
     KMc = dalloc<T>((size_t)Lmid * RP + 2);
@@ -1567,7 +1587,7 @@ struct Engine final : EngineBase {
     k_tri_inv_diag<T><<<1, 64, 0, s4>>>((const T*)Phi, nB, PhiInv, cst, gate_running, k, k);
     ++nlaunch;
     const bool last = k == np - 1;
-    for (int sz = 32; sz < nB; sz *= 2) {
+    for (int sz = 32; sz < tri_cap(); sz *= 2) {
       const int w = sz / 32;  // blocks per half
       if (!last && (k + 1) % (2 * w) != 0) break;  // higher levels end at the same block or later
       const int pair = k / (2 * w);
@@ -1596,7 +1616,7 @@ struct Engine final : EngineBase {
     ph_begin(kPhLU);
     const int nblk = (nB + 31) / 32;
     launch(k_tri_inv_diag<T>, nblk, 64, 0, (const T*)Phi, nB, PhiInv, (const LmDeviceState*)st, gate_running, 0, 200);
-    for (int sz = 32; sz < nB; sz *= 2) {
+    for (int sz = 32; sz < tri_cap(); sz *= 2) {
       const int npairs = (nB + 2 * sz - 1) / (2 * sz);
       const int ks = tri_split(sz);
       const dim3 grid((sz + 63) / 64, (sz + 63) / 64, 2 * npairs * ks);
@@ -1635,6 +1655,31 @@ struct Engine final : EngineBase {
       ph_end();
       return;
     }
+    if (use_blkinv) {
+      const LmDeviceState* cst = st;
+      const int DB = blk_db, nb = (nB + DB - 1) / DB;
+      auto step = [&](auto lower, int b) {
+        constexpr bool LOWER = decltype(lower)::value;
+        const int r0 = b * DB, r1 = std::min(nB, r0 + DB);
+        const int c0 = LOWER ? 0 : r1, c1 = LOWER ? r0 : nB;
+        const unsigned rt = nblocks(r1 - r0, kTmvRows), rs = nblocks(r1 - r0, 256);
+        if (c1 > c0) {  // right-hand side minus the off-diagonal block row times the solved part
+          const unsigned nsl = nblocks(c1 - c0, kTmvCols);
+          launch(k_blk_mv<T, 0>, dim3(rt, nsl), 256, 0, (const T*)Phi, nB, r0, r1, c0, c1, (const T*)xvec, tmv_part, cst,
+                 gate_running);
+          launch(k_blk_sum<T, 0>, rs, 256, 0, (const T*)tmv_part, (int)nsl, nB, r0, r1, xvec, cst, gate_running);
+        }
+        const unsigned nsd = nblocks(r1 - r0, kTmvCols);
+        launch(k_blk_mv<T, LOWER ? 1 : 2>, dim3(rt, nsd), 256, 0, (const T*)PhiInv, nB, r0, r1, r0, r1, (const T*)xvec,
+               tmv_part, cst, gate_running);
+        launch(k_blk_sum<T, LOWER ? 1 : 2>, rs, 256, 0, (const T*)tmv_part, (int)nsd, nB, r0, r1, xvec, cst, gate_running);
+      };
+      for (int b = 0; b < nb; ++b) step(std::true_type{}, b);
+      for (int b = nb - 1; b >= 0; --b) step(std::false_type{}, b);
+      launch(k_apply_k<T>, nblocks(nB, 256), 256, 0, (const T*)xvec, N, R, (const T*)Gp, f, cst, gate_running);
+      ph_end();
+      return;
+    }
     const int nblk = (nB + 31) / 32;
     // ready flags are cleared in-stream (graph-replay safe: no host-side epoch)
     CPF_CUDA_CHECK(cudaMemsetAsync(lu.ticket, 0, sizeof(int) * 2, s));
@@ -1669,9 +1714,9 @@ struct Engine final : EngineBase {
            (const T*)Gp, (const T*)Gf, (const LmDeviceState*)st, gr);
     if (test_singular) launch(k_test_zero_col<T>, 1, 256, 0, Phi, nB, (const LmDeviceState*)st, mode == 1 ? 2 : 1);
     mark(5);
-    lu_factor(gr, use_inv);
+    lu_factor(gr, use_inv || use_blkinv);
     mark(6);
-    if (use_inv && !tri_in_lu) tri_invert(gr);
+    if ((use_inv || use_blkinv) && !tri_in_lu) tri_invert(gr);
     mark(7);
   }
 
@@ -2139,6 +2184,10 @@ struct Engine final : EngineBase {
   }
   void profile(int on) override {
     prof = on != 0;
+    if (prof) for (auto& v : ph_max) v = 0.0;
+  }
+  void phase_max(double* ms, int n) override {
+    for (int i = 0; i < n && i < kNumPhases; ++i) ms[i] = ph_max[i];
   }
   void phase_times(double* ms, int64_t* cnt, int n) override {
     CPF_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -2147,6 +2196,7 @@ struct Engine final : EngineBase {
       CPF_CUDA_CHECK(cudaEventElapsedTime(&t, e.a, e.b));
       ph_ms[e.ph] += t;
       ph_cnt[e.ph] += 1;
+      ph_max[e.ph] = std::max(ph_max[e.ph], (double)t);
       cudaEventDestroy(e.a);
       cudaEventDestroy(e.b);
     }
@@ -2617,6 +2667,11 @@ int cpf_engine_profile(cpf_engine* e, int enable) {
 int cpf_engine_phase_times(cpf_engine* e, double* ms_out, int64_t* counts_out, int nphases) {
   if (!e || !e->impl) return CPF_E_STATE;
   return guarded(e, [&] { e->impl->phase_times(ms_out, counts_out, nphases); });
+}
+
+int cpf_engine_phase_max(cpf_engine* e, double* ms_out, int nphases) {
+  if (!e || !e->impl) return CPF_E_STATE;
+  return guarded(e, [&] { e->impl->phase_max(ms_out, nphases); });
 }
 
 int64_t cpf_engine_launch_count(const cpf_engine* e) { return (e && e->impl) ? e->impl->launches() : 0; }

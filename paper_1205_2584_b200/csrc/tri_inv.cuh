@@ -321,4 +321,61 @@ __global__ void k_tri_mv_sum(const T* __restrict__ part, int nslices, int n, con
   y[i] = v;
 }
 
+// ---- Block-inverse substitution (n_B too large for the full explicit inverse, config 1's 4800)
+// Only the DB x DB diagonal blocks of L and U are inverted (recursive doubling capped at DB / 2), so
+// a triangular solve is ceil(n / DB) block steps of chip-wide mat-vecs instead of a chain of n / 32
+// flag hand-offs between 32-row substitution blocks:
+//   L:  x_b = inv(L_bb) (x_b - L[b, 0:b) x[0:b))        b ascending
+//   U:  x_b = inv(U_bb) (x_b - U[b, b+1:) x[b+1:))      b descending
+// k_blk_mv writes per-(64-row tile, 128-column slice) partial products, k_blk_sum adds the slices
+// in fixed order (deterministic).  MODE 0: full block of the LU factors; 1: unit-lower inverse
+// diagonal block (columns < row); 2: upper inverse diagonal block (columns >= row).
+template <class T, int MODE>
+__global__ void __launch_bounds__(256) k_blk_mv(const T* __restrict__ Mx, int n, int r0, int r1, int c0, int c1,
+                                                const T* __restrict__ x, T* __restrict__ part,
+                                                const LmDeviceState* st, int gate_running) {
+  pdl_wait();
+  if (lu_gated(st, gate_running)) return;
+  __shared__ T red[4][kTmvRows];
+  const int rt = r0 + blockIdx.x * kTmvRows, cs = c0 + blockIdx.y * kTmvCols;
+  const int tid = threadIdx.x, rl = tid % kTmvRows, g = tid / kTmvRows;
+  const int row = rt + rl;
+  T acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = zero_of<T>();
+  const bool tile_live = MODE == 0 ? true : MODE == 1 ? (cs < rt + kTmvRows) : (cs + kTmvCols > rt);
+  if (tile_live && row < r1) {
+    const int cb = cs + g * (kTmvCols / 4);
+#pragma unroll
+    for (int c4 = 0; c4 < kTmvCols / 4; c4 += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = cb + c4 + u;
+        const bool in = c < c1 && (MODE == 0 ? true : MODE == 1 ? c < row : c >= row);
+        if (in) fma_acc(acc[u], Mx[(int64_t)row + (int64_t)n * c], x[c]);
+      }
+    }
+  }
+  T v = acc[0];
+#pragma unroll
+  for (int u = 1; u < 8; ++u) v = add(v, acc[u]);
+  red[g][rl] = v;
+  __syncthreads();
+  if (g == 0 && row < r1) part[(int64_t)blockIdx.y * n + row] = add(add(red[0][rl], red[1][rl]), add(red[2][rl], red[3][rl]));
+}
+
+// MODE 0: x[row] -= sum of slices (right-hand side minus the off-diagonal product); 1: x[row] +=
+// sum (unit-lower inverse block: the implicit diagonal); 2: x[row] = sum (upper inverse block)
+template <class T, int MODE>
+__global__ void k_blk_sum(const T* __restrict__ part, int nslices, int n, int r0, int r1, T* __restrict__ x,
+                          const LmDeviceState* st, int gate_running) {
+  pdl_wait();
+  if (lu_gated(st, gate_running)) return;
+  const int i = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r1) return;
+  T v = zero_of<T>();
+  for (int q = 0; q < nslices; ++q) v = add(v, part[(int64_t)q * n + i]);
+  x[i] = MODE == 0 ? sub(x[i], v) : MODE == 1 ? add(x[i], v) : v;
+}
+
 }  // namespace cpf

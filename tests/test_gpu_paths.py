@@ -47,7 +47,18 @@ def test_complex_register_frame_panel(api):
 
 def test_substitution_solves(api, monkeypatch):
     monkeypatch.setenv("CPF_NO_INV", "1")
+    monkeypatch.setenv("CPF_BLK_INV", "0")
     _check(api, _problem((24, 22, 20), 12, False, 6), 12)  # trsv instead of inv(L), inv(U)
+
+
+@pytest.mark.parametrize("db", [64, 128, 256])
+@pytest.mark.parametrize("complex_", [False, True])
+def test_block_inverse_substitution(api, monkeypatch, db, complex_):
+    """The large-n_B solve path (config 1): inverted diagonal blocks + block steps, forced at
+    n_B = 432 with small blocks (7 / 4 / 2 block steps, ragged last block)."""
+    monkeypatch.setenv("CPF_NO_INV", "1")
+    monkeypatch.setenv("CPF_BLK_DB", str(db))
+    _check(api, _problem((24, 22, 20), 12, complex_, 6), 12)
 
 
 def test_int8_passes_four_way(api, monkeypatch):
