@@ -88,6 +88,13 @@ struct BigCache {
     std::lock_guard<std::mutex> lk(mu());
     bufs().push_back({dev, bytes, p});
   }
+  static size_t parked_bytes(int dev) {
+    std::lock_guard<std::mutex> lk(mu());
+    size_t n = 0;
+    for (const auto& b : bufs())
+      if (b.dev == dev) n += b.bytes;
+    return n;
+  }
   static void release(int dev) {
     std::lock_guard<std::mutex> lk(mu());
     auto& v = bufs();
@@ -803,6 +810,9 @@ struct Engine final : EngineBase {
             cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
           free_b += (size_t)(reserved - used);
       }
+      // so are the tensor-sized buffers an earlier engine of this process parked in the reuse cache
+      // (big_alloc takes them back or releases them): the plan must not depend on what ran before
+      free_b += BigCache::parked_bytes(dev);
       if (!force && need + ((size_t)2 << 30) + (size_t)Jloc * sizeof(T) > free_b) return;
       ozYA = static_cast<uint8_t*>(big_alloc((size_t)oa.ntiles * oa.nkb * kOzABytes, true));
       ozYB = static_cast<uint8_t*>(big_alloc((size_t)ob.ntiles * ob.nkb * kOzABytes, true));
@@ -827,6 +837,9 @@ struct Engine final : EngineBase {
   void plan_spec() {
     use_spec = use_inv && lu3_rpt && (use_oz || !use_dmma);
     if (const char* e = knob("CPF_SPEC")) use_spec = e[0] == '1' && use_inv && lu3_rpt;
+    // the experimental persistent LU's CTAs read the gate state themselves (no latch): never beside
+    // a running k_decide
+    if (lp_cfg) use_spec = false;
     if (!use_spec) return;
     if (const char* e = knob("CPF_SPEC_RESERVE")) kSpecReserveSms = atoi(e);
     if (const char* e = knob("CPF_SPEC_A_SIDE")) spec_a_side = e[0] != '0';
@@ -1459,7 +1472,8 @@ struct Engine final : EngineBase {
       ph_end();
       return;
     }
-    launch(k_lu_init, nblocks(nB, 256), 256, 0, lu.perm, nB, lu.info);
+    launch(k_lu_init, nblocks(nB, 256), 256, 0, lu.perm, nB, lu.info, (const LmDeviceState*)st,
+           gate_running == 3 ? lu.latch : (int*)nullptr);
     if (lu3_rpt) {
       // Look-ahead right-looking LU.  Panel k+1's columns are the "next block" of step k: the
       // panel kernel itself applies step k's interchange and update to them while loading
@@ -1470,7 +1484,6 @@ struct Engine final : EngineBase {
       // and last read the slot panel k overwrites).
       const int KB = kLuMaxKB;
       const int np = (nB + KB - 1) / KB;
-      if (lu.latch) CPF_CUDA_CHECK(cudaMemsetAsync(lu.latch, 0, sizeof(int), s));
       CPF_CUDA_CHECK(cudaEventRecord(evJ, s));
       CPF_CUDA_CHECK(cudaStreamWaitEvent(s2, evJ, 0));
       for (int k = 0; k < np; ++k) {
@@ -1577,12 +1590,65 @@ struct Engine final : EngineBase {
   static constexpr int kTriSplit = 4;
   T* TriPart = nullptr;   // split-K partials: kTriSplit x nB x nB
   T* TriPartS = nullptr;  // the speculative branch's
-  // Progressive form of tri_invert: after the LU's step k (0-based 32-column block k, np blocks)
-  // the blocks 0..k of L and U are final.  Launch on s4 the diagonal inverse of block k and, level
-  // by level, every merge whose pair ends at block k (the last block closes the ragged pairs).
-  // Same kernels, same operation order per output element as the batched launches -> bitwise
-  // identical inverse; only the tail (the pairs that end at the last block) stays behind the LU.
+  // Block step k of the inverse (tri_inv.cuh k_tri_row) on stream strm: the diagonal inverse of
+  // block k, the long products against the leading inverse (split-K with a fixed-order reduce from
+  // 256 leading rows up), then the 32-deep products with the diagonal inverses.  Inside the
+  // look-ahead LU it is launched on s4 right after s2's step k, which finalised blocks 0..k of L
+  // and U -- only the last block's step is left when the factorisation ends.
+  void tri_row_product(int r0, int bs, int base, int tstep, int gate_running, cudaStream_t strm) {
+    const LmDeviceState* cst = st;
+    const int lead = r0 - base;
+    if (lead <= 0) return;
+    const int ks = tri_split(lead);
+    const unsigned ty = (unsigned)((bs + 63) / 64);
+    T* part = ks > 1 ? TriPart : (T*)nullptr;
+    k_tri_row<T, 0><<<dim3((lead + 63) / 64, ty, 2 * ks), 256, 0, strm>>>((const T*)Phi, PhiInv, TriTmp, nB, r0, bs, base, cst,
+                                                                         gate_running, ks, part, tstep);
+    ++nlaunch;
+    if (ks > 1) {
+      const dim3 rgrid(std::max(1, std::min(64, (int)nblocks((int64_t)lead * bs, 256))), 2);
+      k_tri_row_reduce<T><<<rgrid, 256, 0, strm>>>(TriTmp, (const T*)TriPart, ks, nB, r0, bs, base, cst, gate_running, tstep);
+      ++nlaunch;
+    }
+    k_tri_row<T, 1><<<dim3((lead + 63) / 64, ty, 2), 256, 0, strm>>>((const T*)Phi, PhiInv, TriTmp, nB, r0, bs, base, cst,
+                                                                    gate_running, 1, (T*)nullptr, tstep);
+    ++nlaunch;
+  }
+  // rows per group of the two-level schedule (32: every block is its own group).  Groups of 128
+  // make the long products four times rarer; measured at config 4 they still lose to the pair form
+  // (182 vs 188 it/s), so the knob only serves experiments and tests
+  int tri_group() const {
+    if (const char* e = knob("CPF_TRI_GROUP")) return std::max(32, atoi(e) / 32 * 32);
+    return 32;
+  }
+  void tri_row_step(int k, int gate_running, cudaStream_t strm) {
+    const LmDeviceState* cst = st;
+    const int np = (nB + 31) / 32;
+    const int r0 = k * 32, bs = std::min(32, nB - r0);
+    const int cap = tri_cap(), G = tri_group();
+    const int base = (r0 / cap) * cap;      // start of the inverse this block belongs to
+    const int g0 = (r0 / G) * G;            // start of its group
+    k_tri_inv_diag<T><<<1, 64, 0, strm>>>((const T*)Phi, nB, PhiInv, cst, gate_running, k, k);
+    ++nlaunch;
+    tri_row_product(r0, bs, g0, k, gate_running, strm);  // inside the group
+    const int gend = std::min({nB, g0 + G, base + cap});
+    if (r0 + bs >= gend || k == np - 1) tri_row_product(g0, r0 + bs - g0, base, k, gate_running, strm);
+    CPF_CUDA_CHECK(cudaGetLastError());
+  }
+  // which form: rows for the small systems, pairs above (tri_inv.cuh header)
+  bool tri_rows() const {
+    if (const char* e = knob("CPF_TRI_ROWS")) return e[0] == '1';
+    return nB <= 1024;
+  }
   void tri_progress(int k, int np, int gate_running) {
+    if (tri_rows()) tri_row_step(k, gate_running, s4);
+    else tri_pair_progress(k, np, gate_running);
+  }
+  // Pair form (n_B > 1024), progressive: after the LU's step k the blocks 0..k of L and U are final.
+  // Launch on s4 the diagonal inverse of block k and, level by level, every merge whose pair ends
+  // at block k (the last block closes the ragged pairs).  Same kernels and operation order per
+  // output element as the batched launches of tri_invert -> bitwise identical inverse.
+  void tri_pair_progress(int k, int np, int gate_running) {
     const LmDeviceState* cst = st;
     k_tri_inv_diag<T><<<1, 64, 0, s4>>>((const T*)Phi, nB, PhiInv, cst, gate_running, k, k);
     ++nlaunch;
@@ -1614,6 +1680,12 @@ struct Engine final : EngineBase {
   void tri_invert(int gate_running) {
     NvtxRange nvtx_("cpf.tri_inverse");
     ph_begin(kPhLU);
+    if (tri_rows()) {
+      const int np = (nB + 31) / 32;
+      for (int k = 0; k < np; ++k) tri_row_step(k, gate_running, ls);
+      ph_end();
+      return;
+    }
     const int nblk = (nB + 31) / 32;
     launch(k_tri_inv_diag<T>, nblk, 64, 0, (const T*)Phi, nB, PhiInv, (const LmDeviceState*)st, gate_running, 0, 200);
     for (int sz = 32; sz < tri_cap(); sz *= 2) {
@@ -1634,6 +1706,7 @@ struct Engine final : EngineBase {
     }
     ph_end();
   }
+
 
   void apply_b(const T* w, T* f, int gate_running) {
     ph_begin(kPhSolve);

@@ -38,16 +38,24 @@ struct LuWork {
   int* info;       // 1: first zero pivot (1-based), 0 = none
   int* ticket;     // 2 counters for the substitution kernels
   int* ready;      // ceil(n/32) flags
-  int* latch = nullptr;  // speculative branch only: per-panel abandonment latch (panel_gated)
+  int* latch = nullptr;  // speculative branch only: per-panel gate latch (panel_gated)
 };
 
-// Gate of the cluster panel kernels.  Their CTAs synchronise with each other, so all of them must
-// take the same branch; the speculative branch (gate 3) may nevertheless be abandoned between two
-// panels: panel k latches the decision for panel k + 1 (one thread, at its end; the stream order
-// makes it visible and stable for every CTA of the next panel), an abandoned panel passes it on.
+// Gate of the cluster panel kernels.  Their CTAs synchronise with each other (mbarriers, st.async
+// into each other's shared memory), so all of them must take the same branch: a CTA that returned
+// while a peer still waits for its packet hangs the cluster or faults.  The fork's factorisation
+// only reads state that k_decide wrote before the fork started.  The speculative branch (gate 3)
+// runs BESIDE the step's k_decide, which may set `stopped` / the acceptance at any moment -- two
+// CTAs reading the state themselves can disagree (a ~1-in-100-fits hang / launch failure on the
+// last iteration of a fit, found in round 2 by a stress loop).  So in the branch the state is read
+// by ONE thread, ordered before the panel by the stream: k_lu_init latches it for panel 0, panel k
+// latches it for panel k + 1 when it ends, an abandoned panel passes the latch on; the panel's
+// CTAs read only the latch.  This is also what lets the branch's panels be abandoned at all.
+__device__ __forceinline__ int spec_branch_dead(const LmDeviceState* st) {
+  return (st->stopped || st->err_code || ld_volatile_int(&st->accept_iter) == st->spec_iter + 1) ? 1 : 0;
+}
 __device__ __forceinline__ bool panel_gated(const LmDeviceState* st, int gate_running, const LuWork& w, int k) {
-  if (gate_running != 3 || !w.latch) return lu_gated_sync(st, gate_running);
-  if (lu_gated(st, 1)) return true;
+  if (gate_running != 3) return lu_gated_sync(st, gate_running);
   if (w.latch[k]) {
     if (blockIdx.x == 0 && threadIdx.x == 0) w.latch[k + 1] = 1;
     return true;
@@ -55,15 +63,15 @@ __device__ __forceinline__ bool panel_gated(const LmDeviceState* st, int gate_ru
   return false;
 }
 __device__ __forceinline__ void panel_latch_next(const LmDeviceState* st, int gate_running, const LuWork& w, int k) {
-  if (gate_running == 3 && w.latch && blockIdx.x == 0 && threadIdx.x == 0)
-    w.latch[k + 1] = ld_volatile_int(&st->accept_iter) == st->spec_iter + 1 ? 1 : 0;
+  if (gate_running == 3 && blockIdx.x == 0 && threadIdx.x == 0) w.latch[k + 1] = spec_branch_dead(st);
 }
 
-__global__ void k_lu_init(int* perm, int n, int* info) {
+__global__ void k_lu_init(int* perm, int n, int* info, const LmDeviceState* st, int* latch) {
   pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) perm[i] = i;
   if (i == 0) *info = 0;
+  if (i == 0 && latch) latch[0] = spec_branch_dead(st);  // speculative branch: panel_gated
 }
 
 template <class T>

@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
   pdl_wait();
   static_assert(KB == kLuMaxKB, "panel width");
   if (panel_gated(st, gate_running, w, k0 / KB)) return;
+  lu_trace(0, k0 / KB, 0);
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -500,6 +501,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_panel_lu3(T* __restrict__ A, int n,
     }
   }
   cluster.sync();
+  lu_trace(0, k0 / KB, 1);
   panel_latch_next(st, gate_running, w, k0 / KB);
 }
 

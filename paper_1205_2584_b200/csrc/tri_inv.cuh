@@ -6,15 +6,14 @@
 //
 // Storage: Inv (n x n, column-major) holds inv(L) strictly below the diagonal (unit diagonal
 // implicit) and inv(U) on and above it -- the same packing as the LU factors.
-// Algorithm (recursive doubling; batched: every level one launch per product; progressive: each
-// merge launched on a side stream as soon as the LU has finalised its leading block, blk0 / pair0
-// select the block / pair -- engine.cu tri_progress):
-//   level 0: invert every 32x32 diagonal block (one CTA each);
-//   level s: for adjacent blocks (b1, b2) of size s
-//     L: inv([L11 0; L21 L22])  -> X21 = -inv(L22) (L21 inv(L11))
-//     U: inv([U11 U12; 0 U22])  -> X12 = -inv(U11) (U12 inv(U22))
-// Products are 64x64 tiles per CTA, 16 K-rows per smem stage: fp64 on the DMMA tensor pipe,
-// complex128 as DFMA.
+// Algorithm (by block rows of inv(L) / block columns of inv(U), k_tri_row): block k needs the
+// inverse of the leading blocks and block k of the factors, so the engine runs it on a side stream
+// right behind the LU's step k (engine.cu tri_progress) and only the last block's step is left
+// when the factorisation ends.  Used for n_B <= 1024 (config 2: 457 -> 473, config 3: 842 -> 875
+// it/s over the pair form).  For larger systems the chain of per-block long products does not
+// keep up with the panels beside config 4's pass B (measured 180-182 vs 188 it/s), so they use
+// recursive doubling over block pairs (k_tri_level): fewer, larger products, each launched as soon
+// as the LU has finalised the pair; the pairs that end at the last block stay behind the LU.
 #pragma once
 #include "cpf_common.cuh"
 
@@ -80,43 +79,28 @@ __device__ __forceinline__ T tri_elem(const T* M, int n, int r, int c, int kind)
   return M[(int64_t)r + (int64_t)n * c];
 }
 
-// One level product for every (pair, triangle): C = alpha * opA(A) * opB(B), all blocks inside
-// n x n column-major matrices.  blockIdx.z = (2 * pair + tri) * ksplit + ks (tri 0: L, 1: U).
-// Split-K (ksplit > 1, the large levels): split ks covers its share of the (triangle-skipped) K
-// range and writes alpha * partial into part[ks] (n x n layout); k_tri_reduce adds the ksplit
-// partials in fixed order -- deterministic.  The large levels have few output tiles and K up to
-// n: without the split a handful of CTAs run 1024-deep K loops (ncu: ~100 us per launch at
-// n_B = 1200, issue 18-22 %).
-//   step 0 (T):  L: T[b2,b1] = L21 * inv(L11)      U: T[b1,b2] = U12 * inv(U22)
-//   step 1 (X):  L: X[b2,b1] = -inv(L22) * T        U: X[b1,b2] = -inv(U11) * T
-template <class T, int STEP>
-__global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* __restrict__ Inv, T* __restrict__ Tmp,
-                                                   int n, int s, const LmDeviceState* st, int gate_running,
-                                                   int ksplit, T* __restrict__ part, int pair0, int tstep) {
-  pdl_wait();
-  if (lu_gated(st, gate_running)) return;
-  const int ks = blockIdx.z % ksplit, pt = blockIdx.z / ksplit;
-  const int pair = pair0 + (pt >> 1), tri = pt & 1;
-  const int b1 = 2 * pair * s, b2 = b1 + s;
-  if (b2 >= n) return;
-  const int s1 = s, s2 = min(s, n - b2);
-  // output block: rows/cols and operands
-  int m, nn, kk, ra, ca, rb, cb, rc, cc, kindA, kindB;
-  const T *Am, *Bm;
-  T* Cm;
+// One product C = alpha * opA(A) * opB(B) of the block inverse, all blocks inside n x n column-major
+// matrices; a CTA computes one 64x64 tile (fp64 on the DMMA tensor pipe, complex128 as DFMA; 16
+// K-rows per smem stage).  Triangular operands skip the K range that only multiplies zeros.
+// Split-K (ksplit > 1): split ks covers its share of the K range and writes alpha * partial into
+// part[ks] (n x n layout); the reduce kernel adds the partials in fixed order -- deterministic.
+template <class T>
+struct TriProd {
+  int m, nn, kk;            // C is m x nn, inner dimension kk
+  const T* Am; int ra, ca, kindA;
+  const T* Bm; int rb, cb, kindB;
+  T* Cm; int rc, cc;
   double alpha;
-  if (tri == 0) {  // L
-    m = s2; nn = s1;
-    if (STEP == 0) { kk = s1; Am = LU; ra = b2; ca = b1; kindA = kOpFull; Bm = Inv; rb = b1; cb = b1; kindB = kOpInvL; alpha = 1.0; Cm = Tmp; }
-    else { kk = s2; Am = Inv; ra = b2; ca = b2; kindA = kOpInvL; Bm = Tmp; rb = b2; cb = b1; kindB = kOpFull; alpha = -1.0; Cm = Inv; }
-    rc = b2; cc = b1;
-  } else {  // U
-    m = s1; nn = s2;
-    if (STEP == 0) { kk = s2; Am = LU; ra = b1; ca = b2; kindA = kOpFull; Bm = Inv; rb = b2; cb = b2; kindB = kOpInvU; alpha = 1.0; Cm = Tmp; }
-    else { kk = s1; Am = Inv; ra = b1; ca = b1; kindA = kOpInvU; Bm = Tmp; rb = b1; cb = b2; kindB = kOpFull; alpha = -1.0; Cm = Inv; }
-    rc = b1; cc = b2;
-  }
-  const int tm = blockIdx.x * 64, tn = blockIdx.y * 64;
+};
+
+template <class T>
+__device__ __forceinline__ void tri_tile_product(const TriProd<T>& q, int n, int tm, int tn, int ks, int ksplit,
+                                                 T* __restrict__ part, int tstep) {
+  const int m = q.m, nn = q.nn, kk = q.kk, ra = q.ra, ca = q.ca, rb = q.rb, cb = q.cb, rc = q.rc, cc = q.cc;
+  const int kindA = q.kindA, kindB = q.kindB;
+  const T *Am = q.Am, *Bm = q.Bm;
+  T* Cm = q.Cm;
+  const double alpha = q.alpha;
   if (tm >= m || tn >= nn) return;
   lu_trace(1, 256 + tstep, 0);
   constexpr int KS = 16 * 8 / (int)sizeof(T);  // K rows per stage (8 for complex: 48 KB static smem)
@@ -133,9 +117,7 @@ __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* 
     kend = min(kend, lo + per);
     kbeg = lo;
   }
-  if (ksplit > 1) {
-    Cm = part + (size_t)ks * n * n;
-  }
+  if (ksplit > 1) Cm = part + (size_t)ks * n * n;
   __shared__ T As[2][KS][64 + 1];
   __shared__ T Bs[2][KS][64 + 1];
   const int tid = threadIdx.x;
@@ -245,6 +227,95 @@ __global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* 
       }
     lu_trace(1, 256 + tstep, 1);
   }
+}
+
+// Row-by-row form of the inverse (the order LAPACK's trtri uses, by block rows / columns): once the
+// LU has finalised block k (rows/columns [r0, r0 + bs)), with the inverse of the leading part
+// [base, r0) of its diagonal block already in Inv,
+//   L:  Inv[k, base:r0] = -inv(L_kk) (L[k, base:r0] inv(L)[base:r0, base:r0])
+//   U:  Inv[base:r0, k] = -(inv(U)[base:r0, base:r0] U[base:r0, k]) inv(U_kk)
+// STEP 0 is the long product (K = r0 - base, needs only the leading inverse: it can run while the
+// diagonal block is still being inverted), STEP 1 the bs-deep one.  blockIdx.x: 64-wide tile along
+// the leading part, blockIdx.y: 64-wide tile along the block, blockIdx.z = tri * ksplit + ks (tri 0:
+// L, 1: U).  The engine applies it at two granularities (tri_row_step): every 32-row LU block
+// against the start of its group of G rows, and every completed group (bs = G) against the start of
+// the inverse (base = 0: full inverse; the DB x DB diagonal block: block-inverse substitution).
+template <class T, int STEP>
+__global__ void __launch_bounds__(256) k_tri_row(const T* __restrict__ LU, T* __restrict__ Inv, T* __restrict__ Tmp,
+                                                 int n, int r0, int bs, int base, const LmDeviceState* st,
+                                                 int gate_running, int ksplit, T* __restrict__ part, int tstep) {
+  pdl_wait();
+  if (lu_gated(st, gate_running)) return;
+  const int ks = blockIdx.z % ksplit, tri = blockIdx.z / ksplit;
+  const int lead = r0 - base;
+  TriProd<T> q;
+  int tm, tn;
+  if (tri == 0) {
+    q.m = bs; q.nn = lead; tm = blockIdx.y * 64; tn = blockIdx.x * 64;
+    if (STEP == 0) { q.kk = lead; q.Am = LU; q.ra = r0; q.ca = base; q.kindA = kOpFull; q.Bm = Inv; q.rb = base; q.cb = base; q.kindB = kOpInvL; q.Cm = Tmp; q.alpha = 1.0; }
+    else { q.kk = bs; q.Am = Inv; q.ra = r0; q.ca = r0; q.kindA = kOpInvL; q.Bm = Tmp; q.rb = r0; q.cb = base; q.kindB = kOpFull; q.Cm = Inv; q.alpha = -1.0; }
+    q.rc = r0; q.cc = base;
+  } else {
+    q.m = lead; q.nn = bs; tm = blockIdx.x * 64; tn = blockIdx.y * 64;
+    if (STEP == 0) { q.kk = lead; q.Am = Inv; q.ra = base; q.ca = base; q.kindA = kOpInvU; q.Bm = LU; q.rb = base; q.cb = r0; q.kindB = kOpFull; q.Cm = Tmp; q.alpha = 1.0; }
+    else { q.kk = bs; q.Am = Tmp; q.ra = base; q.ca = r0; q.kindA = kOpFull; q.Bm = Inv; q.rb = r0; q.cb = r0; q.kindB = kOpInvU; q.Cm = Inv; q.alpha = -1.0; }
+    q.rc = base; q.cc = r0;
+  }
+  tri_tile_product(q, n, tm, tn, ks, ksplit, part, tstep);
+}
+
+// Sum of the split-K partials of a row step's long product (fixed order) into Tmp.  grid.y = 2.
+template <class T>
+__global__ void k_tri_row_reduce(T* __restrict__ Tmp, const T* __restrict__ part, int ksplit, int n, int r0, int bs,
+                                 int base, const LmDeviceState* st, int gate_running, int tstep) {
+  pdl_wait();
+  if (lu_gated(st, gate_running)) return;
+  const int tri = blockIdx.y, lead = r0 - base;
+  const int rc = tri == 0 ? r0 : base, cc = tri == 0 ? base : r0;
+  const int m = tri == 0 ? bs : lead, nn = tri == 0 ? lead : bs;
+  const size_t nn2 = (size_t)n * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)m * nn; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % m), c = (int)(e / m);
+    const size_t off = (size_t)(rc + r) + (size_t)n * (cc + c);
+    T v = part[off];
+    for (int k = 1; k < ksplit; ++k) v = add(v, part[(size_t)k * nn2 + off]);
+    Tmp[off] = v;
+  }
+  lu_trace(1, 256 + tstep, 1);
+}
+
+// Recursive doubling over adjacent block pairs (the form used for n_B > 1024, where a chain of
+// per-block products does not keep up with the panels beside config 4's pass B): level s merges
+// blocks (b1, b2) of size s
+//     L: inv([L11 0; L21 L22])  -> X21 = -inv(L22) (L21 inv(L11))
+//     U: inv([U11 U12; 0 U22])  -> X12 = -inv(U11) (U12 inv(U22))
+// blockIdx.z = (2 * (pair - pair0) + tri) * ksplit + ks (tri 0: L, 1: U).
+//   step 0 (T):  L: T[b2,b1] = L21 * inv(L11)      U: T[b1,b2] = U12 * inv(U22)
+//   step 1 (X):  L: X[b2,b1] = -inv(L22) * T        U: X[b1,b2] = -inv(U11) * T
+template <class T, int STEP>
+__global__ void __launch_bounds__(256) k_tri_level(const T* __restrict__ LU, T* __restrict__ Inv, T* __restrict__ Tmp,
+                                                   int n, int s, const LmDeviceState* st, int gate_running,
+                                                   int ksplit, T* __restrict__ part, int pair0, int tstep) {
+  pdl_wait();
+  if (lu_gated(st, gate_running)) return;
+  const int ks = blockIdx.z % ksplit, pt = blockIdx.z / ksplit;
+  const int pair = pair0 + (pt >> 1), tri = pt & 1;
+  const int b1 = 2 * pair * s, b2 = b1 + s;
+  if (b2 >= n) return;
+  const int s1 = s, s2 = min(s, n - b2);
+  TriProd<T> q;
+  if (tri == 0) {  // L
+    q.m = s2; q.nn = s1;
+    if (STEP == 0) { q.kk = s1; q.Am = LU; q.ra = b2; q.ca = b1; q.kindA = kOpFull; q.Bm = Inv; q.rb = b1; q.cb = b1; q.kindB = kOpInvL; q.alpha = 1.0; q.Cm = Tmp; }
+    else { q.kk = s2; q.Am = Inv; q.ra = b2; q.ca = b2; q.kindA = kOpInvL; q.Bm = Tmp; q.rb = b2; q.cb = b1; q.kindB = kOpFull; q.alpha = -1.0; q.Cm = Inv; }
+    q.rc = b2; q.cc = b1;
+  } else {  // U
+    q.m = s1; q.nn = s2;
+    if (STEP == 0) { q.kk = s2; q.Am = LU; q.ra = b1; q.ca = b2; q.kindA = kOpFull; q.Bm = Inv; q.rb = b2; q.cb = b2; q.kindB = kOpInvU; q.alpha = 1.0; q.Cm = Tmp; }
+    else { q.kk = s1; q.Am = Inv; q.ra = b1; q.ca = b1; q.kindA = kOpInvU; q.Bm = Tmp; q.rb = b1; q.cb = b2; q.kindB = kOpFull; q.alpha = -1.0; q.Cm = Inv; }
+    q.rc = b1; q.cc = b2;
+  }
+  tri_tile_product(q, n, (int)blockIdx.x * 64, (int)blockIdx.y * 64, ks, ksplit, part, tstep);
 }
 
 // Sum of the split-K partials of one level (fixed order) into its output blocks: STEP 0 -> Tmp,

@@ -70,3 +70,15 @@ def test_int8_passes_four_way(api, monkeypatch):
 def test_int8_passes_order_2_and_5(api, monkeypatch, dims, R):
     monkeypatch.setenv("CPF_OZ", "1")
     _check(api, _problem(dims, R, False, 8), R)
+
+
+@pytest.mark.parametrize("env", [{"CPF_TRI_ROWS": "1"}, {"CPF_TRI_ROWS": "1", "CPF_TRI_GROUP": "128"},
+                                 {"CPF_TRI_ROWS": "0"}, {"CPF_TRI_ROWS": "0", "CPF_TRI_PROG": "0"},
+                                 {"CPF_TRI_ROWS": "1", "CPF_TRI_PROG": "0"}])
+@pytest.mark.parametrize("complex_", [False, True])
+def test_inverse_forms(api, monkeypatch, env, complex_):
+    """Both forms of the explicit triangular inverse (block rows / block pairs), progressive and
+    batched, on a multi-panel core system (n_B = 432, ragged last block)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _check(api, _problem((24, 22, 20), 12, complex_, 6), 12)

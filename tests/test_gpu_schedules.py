@@ -77,3 +77,25 @@ def test_repeated_fits_bitwise(api, monkeypatch, case):
     for _ in range(9):
         tr, v = _run(api, monkeypatch, case, {"CPF_SPEC": "1"})
         assert tr == base_tr and np.array_equal(v, base_v)
+
+
+@pytest.mark.parametrize("env", [{}, {"CPF_TRI_ROWS": "0"}])
+def test_many_full_c2_fits_do_not_fault(api, monkeypatch, env):
+    """Config 2 at full size (n_B = 900: two-CTA cluster panels, speculative branch on), 60 fits in
+    one process.  The branch's panels run beside k_decide; before their gate was latched by a single
+    thread (lu.cuh panel_gated) about one fit in a hundred hung or faulted on its last iteration,
+    when two CTAs of a cluster read `stopped` on either side of k_decide's write."""
+    from paper_1205_2584_b200 import synth
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = synth.CONFIGS["c2"]
+    y = synth.make_tensor(cfg, 0)
+    tau = synth.tau_for_unit_mu(cfg, 0)
+    base = None
+    for _ in range(60):
+        res = api.fit(y, api.FitConfig(rank=cfg.rank, tau=tau, tol=0.0, max_iters=cfg.max_iters, seed=0, init="random"))
+        sig = ([(r.iter, r.relerr, r.mu, r.accepted) for r in res.trace], res.final_relerr)
+        if base is None:
+            base = sig
+        assert sig == base
