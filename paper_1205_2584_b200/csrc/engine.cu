@@ -263,7 +263,7 @@ struct Engine final : EngineBase {
   // CPF_MARKS=3: the marks are external event-record nodes of the captured iteration graph, read
   // after every replay (graph-mode section times; diagnostic, one replay per poll)
   const bool gmarks = [] { const char* e = knob("CPF_MARKS"); return e && e[0] == '3'; }();
-  cudaEvent_t gmark[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t gmark[9] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   bool capturing = false;
   void mark(int id) {
     if (spec_capture) return;
@@ -1473,7 +1473,7 @@ struct Engine final : EngineBase {
       return;
     }
     launch(k_lu_init, nblocks(nB, 256), 256, 0, lu.perm, nB, lu.info, (const LmDeviceState*)st,
-           gate_running == 3 ? lu.latch : (int*)nullptr);
+           gate_running == 3 ? lu.latch : (int*)nullptr, gate_running);
     if (lu3_rpt) {
       // Look-ahead right-looking LU.  Panel k+1's columns are the "next block" of step k: the
       // panel kernel itself applies step k's interchange and update to them while loading
@@ -2058,76 +2058,65 @@ struct Engine final : EngineBase {
     CPF_CUDA_CHECK(cudaStreamSynchronize(s));
     hst->use_kinv = tmp.use_kinv;
     CPF_CUDA_CHECK(cudaMemcpyAsync(st, hst, sizeof(LmDeviceState), cudaMemcpyHostToDevice, s));
-    prepare_core(kRunning);  // Phi(mu_0, cache_0) for the first iteration
+    if (!rotated()) prepare_core(kRunning);  // else Phi(mu_0, cache_0) is factored by the first unit's fork
     CPF_CUDA_CHECK(cudaStreamSynchronize(s));
     fill_status(o);
   }
 
   static constexpr int kStopMaxIters = 4;
 
-  void iteration() {
-    NvtxRange nvtx_("cpf.iteration (eager or captured)");
-    const int g = kRunning;
-    pdl_now = true;
-    mark(0);
-    if (use_spec) {
-      // the previous step was rejected: its core system is the speculated one
-      const int gp = kOnRejectPrev;
-      launch(k_copy<T>, nblocks((int64_t)nB * nB, 256), 256, 0, (const T*)PhiInvS, PhiInv, (int64_t)nB * nB,
-             (const LmDeviceState*)st, (const DevFlags*)fl, gp);
-      launch(k_copy<int>, nblocks(nB, 256), 256, 0, (const int*)luS.perm, lu.perm, (int64_t)nB,
-             (const LmDeviceState*)st, (const DevFlags*)fl, gp);
-      launch(k_copy<T>, nblocks((int64_t)N * R * R, 256), 256, 0, (const T*)GtiS, Gti, (int64_t)N * R * R,
-             (const LmDeviceState*)st, (const DevFlags*)fl, gp);
-      launch(k_copy<T>, nblocks((int64_t)N * R * R, 256), 256, 0, (const T*)GiS, Gi, (int64_t)N * R * R,
-             (const LmDeviceState*)st, (const DevFlags*)fl, gp);
-      launch(k_spec_errors, 1, 1, 0, st, (const DevFlags*)fl, (const int*)spec_sing, (const int*)luS.info);
-      // this step's rejection branch, beside the candidate and pass A; its mu is snapshotted on s
-      // (ordered before this iteration's k_decide), the branch itself only reads dscal[8]
-      launch(k_spec_begin, 1, 1, 0, st, dscal + 8, spec_sing);
-      CPF_CUDA_CHECK(cudaEventRecord(evS0, s));
-      CPF_CUDA_CHECK(cudaStreamWaitEvent(sS, evS0, 0));
-      pdl_now = false;
-      spec_capture = true;
-      swap_spec();
-      ls = s;
-      prepare_core(g, 1);
-      CPF_CUDA_CHECK(cudaEventRecord(evS1, s));
-      swap_spec();
-      ls = s;
-      spec_capture = false;
-      pdl_now = true;
-    }
-    candidate(2, g, /*core_ready=*/true);  // Phi(mu_t, cache_t) was factored at the end of t-1
-    mark(1);
-    // delta' = cand - model (solver.py:348)
-    axpby(Cand, 1.0, A, -1.0, V1, g);
-    // normalised candidate: trial fit and, if accepted, the new model (solver.py:362)
-    normalize(Cand, Ac, g, 1);
-    cross_gram(Ac, Ac, Ccg, g);
-    launch(k_xnorm2<T>, 1, 256, 0, (const T*)Ccg, N, R, dscal + 2, (const LmDeviceState*)st, (const DevFlags*)fl, g);
-    pass_a(Ac, Mc, g);
-    launch(k_redot<T>, 1, 1024, 0, (const T*)(Ac + offs[0]), (const T*)(Mc + offs[0]), I1 * R, 0, dscal + 0,
-           (const LmDeviceState*)st, (const DevFlags*)fl, g);
-    launch(k_redot<T>, 1, 1024, 0, (const T*)V1, (const T*)G, RT, 1, dscal + 3, (const LmDeviceState*)st,
-           (const DevFlags*)fl, g);
-    launch(k_precheck, 1, 1, 0, (const LmDeviceState*)st, fl, (const double*)dscal);
-    direct_resid(Ac, dscal + 4, kOnDirect);
-    direct_resid(A, dscal + 5, kOnCurDirect);
-    launch(k_decide, 1, 1, 0, st, fl, dtrace, (const double*)dscal);
-    mark(2);
-    // commit an accepted candidate (solver.py:361-367): model, cache, MTTKRPs, gradient
-    const int ga = kOnAccept;
-    launch(k_copy<T>, nblocks(RT, 256), 256, 0, (const T*)Ac, A, RT, (const LmDeviceState*)st, (const DevFlags*)fl, ga);
-    launch(k_copy<T>, nblocks((int64_t)N * R * R, 256), 256, 0, (const T*)Ccg, Cg, (int64_t)N * R * R,
-           (const LmDeviceState*)st, (const DevFlags*)fl, ga);
-    cache_from_grams(Cg, ga);
-    launch(k_copy<T>, nblocks(offs[N - 1], 256), 256, 0, (const T*)Mc, M, offs[N - 1], (const LmDeviceState*)st,
-           (const DevFlags*)fl, ga);
-    // fork: pass B (M_N of the new model) + gradient on s3, while s factors the next step's
-    // core system Phi(mu_{t+1}, cache_{t+1}) -- independent of Y, so the two overlap
+  // One replay unit, in one of two orders.
+  //   rotated (the FMA-pass configurations): fork -> step.  The unit starts at the fork that follows
+  //     the previous decision (first iteration: only the core system) and ends with this
+  //     iteration's decision and commit.  The step's rejection branch Phi(cache_t, mu_t * growth_t)
+  //     -- known as soon as the previous decision is -- is launched BEFORE the fork, so it has
+  //     the whole unit (fork + candidate + pass A): a rejection right after an accepted step no
+  //     longer waits for most of the speculated factorisation, and a fit does not end with a
+  //     fork nobody needs.
+  //   classic (int8 passes, config 4): step -> fork, the branch beside candidate + pass A only.
+  //     Measured there: two factorisations beside pass B share its 40 SMs (173 it/s), and with
+  //     the branch after the fork the unit ends with the drain of an abandoned branch's ~250
+  //     gated kernels, which the classic order hides inside the fork (163 vs 185 it/s).
+  //   fork   accepted previous step: pass B (M_N of the new model) + gradient on s3, beside the
+  //          core system Phi(mu_t, cache_t), its LU and inverse on s (independent of Y);
+  //          after a rho <= 0 rejection nothing (the speculated system is copied in)
+  //   step   candidate -> normalise -> pass A -> trial fit -> decide -> commit
+  bool rotated() const {
+    if (const char* e = knob("CPF_ROTATED")) return e[0] == '1';
+    return !use_oz;
+  }
+  void spec_launch(int g) {
+    // the previous step was rejected: its core system is the speculated one
+    const int gp = kOnRejectPrev;
+    launch(k_copy<T>, nblocks((int64_t)nB * nB, 256), 256, 0, (const T*)PhiInvS, PhiInv, (int64_t)nB * nB,
+           (const LmDeviceState*)st, (const DevFlags*)fl, gp);
+    launch(k_copy<int>, nblocks(nB, 256), 256, 0, (const int*)luS.perm, lu.perm, (int64_t)nB,
+           (const LmDeviceState*)st, (const DevFlags*)fl, gp);
+    launch(k_copy<T>, nblocks((int64_t)N * R * R, 256), 256, 0, (const T*)GtiS, Gti, (int64_t)N * R * R,
+           (const LmDeviceState*)st, (const DevFlags*)fl, gp);
+    launch(k_copy<T>, nblocks((int64_t)N * R * R, 256), 256, 0, (const T*)GiS, Gi, (int64_t)N * R * R,
+           (const LmDeviceState*)st, (const DevFlags*)fl, gp);
+    launch(k_spec_errors, 1, 1, 0, st, (const DevFlags*)fl, (const int*)spec_sing, (const int*)luS.info);
+    // its mu is snapshotted on s (ordered before this iteration's k_decide), the branch itself only
+    // reads dscal[8]
+    launch(k_spec_begin, 1, 1, 0, st, dscal + 8, spec_sing);
+    CPF_CUDA_CHECK(cudaEventRecord(evS0, s));
+    CPF_CUDA_CHECK(cudaStreamWaitEvent(sS, evS0, 0));
+    const bool pdl_prev = pdl_now;
     pdl_now = false;
-    mark(3);
+    spec_capture = true;
+    swap_spec();
+    ls = s;
+    prepare_core(g, 1);
+    CPF_CUDA_CHECK(cudaEventRecord(evS1, s));
+    swap_spec();
+    ls = s;
+    spec_capture = false;
+    pdl_now = pdl_prev;
+  }
+  void fork_core(int g) {
+    const int ga = kOnAccept;
+    pdl_now = false;
     if (serial) {  // diagnostic (CPF_SERIAL=1): no overlap, phases time standalone
       pass_b(A, M, ga);
       gradient(ga);
@@ -2144,8 +2133,53 @@ struct Engine final : EngineBase {
       CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evG, 0));
     }
     launch(k_clear_pending, 1, 1, 0, fl);
-    if (use_spec) CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evS1, 0));
+    pdl_now = true;
+  }
+
+  void iteration() {
+    NvtxRange nvtx_("cpf.iteration (eager or captured)");
+    const int g = kRunning;
+    pdl_now = true;
+    mark(0);
+    if (rotated()) {
+      if (use_spec) spec_launch(g);
+      fork_core(g);
+    } else if (use_spec) {
+      spec_launch(g);
+    }
+    mark(1);
+    candidate(2, g, /*core_ready=*/true);  // Phi(mu_t, cache_t): factored in the fork or speculated
+    mark(2);
+    // delta' = cand - model (solver.py:348)
+    axpby(Cand, 1.0, A, -1.0, V1, g);
+    // normalised candidate: trial fit and, if accepted, the new model (solver.py:362)
+    normalize(Cand, Ac, g, 1);
+    cross_gram(Ac, Ac, Ccg, g);
+    launch(k_xnorm2<T>, 1, 256, 0, (const T*)Ccg, N, R, dscal + 2, (const LmDeviceState*)st, (const DevFlags*)fl, g);
+    pass_a(Ac, Mc, g);
+    launch(k_redot<T>, 1, 1024, 0, (const T*)(Ac + offs[0]), (const T*)(Mc + offs[0]), I1 * R, 0, dscal + 0,
+           (const LmDeviceState*)st, (const DevFlags*)fl, g);
+    launch(k_redot<T>, 1, 1024, 0, (const T*)V1, (const T*)G, RT, 1, dscal + 3, (const LmDeviceState*)st,
+           (const DevFlags*)fl, g);
+    launch(k_precheck, 1, 1, 0, (const LmDeviceState*)st, fl, (const double*)dscal);
+    direct_resid(Ac, dscal + 4, kOnDirect);
+    direct_resid(A, dscal + 5, kOnCurDirect);
+    launch(k_decide, 1, 1, 0, st, fl, dtrace, (const double*)dscal);
+    mark(3);
+    // commit an accepted candidate (solver.py:361-367): model, cache, MTTKRPs; M_N and the gradient
+    // follow in the next unit's fork
+    const int ga = kOnAccept;
+    launch(k_copy<T>, nblocks(RT, 256), 256, 0, (const T*)Ac, A, RT, (const LmDeviceState*)st, (const DevFlags*)fl, ga);
+    launch(k_copy<T>, nblocks((int64_t)N * R * R, 256), 256, 0, (const T*)Ccg, Cg, (int64_t)N * R * R,
+           (const LmDeviceState*)st, (const DevFlags*)fl, ga);
+    cache_from_grams(Cg, ga);
+    launch(k_copy<T>, nblocks(offs[N - 1], 256), 256, 0, (const T*)Mc, M, offs[N - 1], (const LmDeviceState*)st,
+           (const DevFlags*)fl, ga);
+    pdl_now = false;
     mark(4);
+    if (!rotated()) fork_core(g);
+    if (use_spec) CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evS1, 0));
+    mark(8);
   }
 
   void capture_iteration() {
@@ -2188,13 +2222,16 @@ struct Engine final : EngineBase {
       }
       k += batch;
       pull_state();
-      if (use_graph && gmarks && gmark[0] && gmark[4]) {
-        float t[4];
+      if (use_graph && gmarks && gmark[0] && gmark[4] && gmark[8]) {
+        // sections: [rotated: branch launch + fork | else branch launch] | candidate | normalise +
+        // pass A + decide | commit | [classic: fork] + join of the branch
+        float t[5];
         for (int i = 0; i < 4; ++i) CPF_CUDA_CHECK(cudaEventElapsedTime(&t[i], gmark[i], gmark[i + 1]));
-        fprintf(stderr, "[cpf graph iter] %.3f %.3f %.3f %.3f", t[0], t[1], t[2], t[3]);
-        if (gmark[5] && gmark[6] && gmark[7]) {  // inside the fork: core prep | LU | inverse (from mark 3)
+        CPF_CUDA_CHECK(cudaEventElapsedTime(&t[4], gmark[4], gmark[8]));
+        fprintf(stderr, "[cpf graph iter] %.3f %.3f %.3f %.3f %.3f", t[0], t[1], t[2], t[3], t[4]);
+        if (gmark[5] && gmark[6] && gmark[7]) {  // inside the fork: core prep | LU | inverse
           float u[3];
-          CPF_CUDA_CHECK(cudaEventElapsedTime(&u[0], gmark[3], gmark[5]));
+          CPF_CUDA_CHECK(cudaEventElapsedTime(&u[0], gmark[rotated() ? 0 : 4], gmark[5]));
           CPF_CUDA_CHECK(cudaEventElapsedTime(&u[1], gmark[5], gmark[6]));
           CPF_CUDA_CHECK(cudaEventElapsedTime(&u[2], gmark[6], gmark[7]));
           fprintf(stderr, "  | core prep %.3f LU %.3f inverse %.3f", u[0], u[1], u[2]);
@@ -2288,7 +2325,7 @@ struct Engine final : EngineBase {
     marks.clear();
     if (const char* e = knob("CPF_MARKS"))
       if (e[0] == '1')
-        fprintf(stderr, "[cpf marks] candidate %.3f  passA+decide %.3f  commit %.3f  fork %.3f ms (totals)\n",
+        fprintf(stderr, "[cpf marks] branch launch (+ fork, rotated) %.3f  candidate %.3f  passA+decide %.3f  commit %.3f ms (totals)\n",
                 mark_ms[0], mark_ms[1], mark_ms[2], mark_ms[3]);
     for (int i = 0; i < n && i < kNumPhases; ++i) {
       ms[i] = ph_ms[i];

@@ -66,12 +66,15 @@ __device__ __forceinline__ void panel_latch_next(const LmDeviceState* st, int ga
   if (gate_running == 3 && blockIdx.x == 0 && threadIdx.x == 0) w.latch[k + 1] = spec_branch_dead(st);
 }
 
-__global__ void k_lu_init(int* perm, int n, int* info, const LmDeviceState* st, int* latch) {
+__global__ void k_lu_init(int* perm, int n, int* info, const LmDeviceState* st, int* latch, int gate_running) {
   pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0 && latch) latch[0] = spec_branch_dead(st);  // speculative branch: panel_gated
+  // a gated factorisation leaves the permutation alone: after a rho <= 0 rejection it is the
+  // speculated system's, copied in at the start of the replay unit
+  if (lu_gated(st, gate_running)) return;
   if (i < n) perm[i] = i;
   if (i == 0) *info = 0;
-  if (i == 0 && latch) latch[0] = spec_branch_dead(st);  // speculative branch: panel_gated
 }
 
 template <class T>

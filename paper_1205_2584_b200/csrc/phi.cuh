@@ -22,7 +22,7 @@ __global__ void k_phi_assemble(T* __restrict__ Phi, int N, int R, const T* __res
   pdl_wait();
   if (gate_running && st->stopped) return;
   if (st->err_code) return;
-  if (gate_running == 2 && !st->accepted) return;
+  if (gate_running == 2 && st->rej_grow) return;  // after a rho <= 0 rejection the speculated system is used
   if (lu_gated(st, gate_running == 3 ? 3 : 0)) return;
   const int R2 = R * R;
   const int64_t nB = (int64_t)N * R2;

@@ -1,5 +1,6 @@
 """Per-iteration section times of a config-4 fit: eager, profiled (CPF_MARKS=2) or graph replay (CPF_MARKS=3):
-candidate | normalise + pass A + trial fit + decide | commit | fork (pass B || next core) -> join."""
+[rotated order: branch launch + fork (pass B || this step's core system)] | candidate | normalise +
+pass A + trial fit + decide | commit | [classic order: fork] + join of the speculated branch."""
 import os as _os
 _os.environ.setdefault("CPF_DEBUG", "1")  # engine knobs are read only under CPF_DEBUG=1
 import os
