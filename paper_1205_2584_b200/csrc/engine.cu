@@ -899,15 +899,53 @@ struct Engine final : EngineBase {
   // Accuracy guard (tensor_pass_oz.cuh): if any row of either pass's view of Y is outside the int8
   // split's envelope, the engine drops the int8 passes for this tensor and stays on fp64.
   bool oz_y_rejected = false;
-  void oz_split() {
+  // Host upload of a large real tensor in slices of the last mode, with the pass-B image built
+  // behind it: a pass-B tile row (i1, c) is complete once slice c has arrived, so its row exponents
+  // and digit planes are computed on s3 while the next slices cross PCIe (the pass-A rows span all
+  // c and wait for the whole tensor).  Same kernels on tile ranges: identical image bytes.
+  // Returns false (nothing done) when the plan does not apply.
+  bool upload_with_split(const void* p) {
+    if constexpr (sizeof(T) != 8) return false;
+    else {
+      if (!use_oz || Cloc < 16 || Jloc < ((int64_t)1 << 27)) return false;
+      if (const char* e = knob("CPF_UPLOAD_SPLIT")) if (e[0] == '0') return false;
+      const double* Yd = reinterpret_cast<const double*>(Yown);
+      int* ybad = reinterpret_cast<int*>(red);  // scratch
+      CPF_CUDA_CHECK(cudaMemsetAsync(ybad, 0, sizeof(int), s));
+      const int nchunk = 8;
+      const int64_t per = (Cloc + nchunk - 1) / nchunk, slice = Lrows;
+      cudaEvent_t ev = nullptr, evEnd = nullptr;
+      CPF_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CPF_CUDA_CHECK(cudaEventCreateWithFlags(&evEnd, cudaEventDisableTiming));
+      for (int64_t c0 = 0; c0 < Cloc; c0 += per) {
+        const int64_t c1 = std::min(Cloc, c0 + per);
+        CPF_CUDA_CHECK(cudaMemcpyAsync(Yown + c0 * slice, static_cast<const T*>(p) + c0 * slice,
+                                       (size_t)((c1 - c0) * slice) * sizeof(T), cudaMemcpyHostToDevice, s));
+        CPF_CUDA_CHECK(cudaEventRecord(ev, s));
+        CPF_CUDA_CHECK(cudaStreamWaitEvent(s3, ev, 0));
+        // pass-B tiles t = c * nb + b of the slices [c0, c1)
+        k_oz_rowexp<1><<<nsm_ * 2, 256, 0, s3>>>(Yd, ob, ozFrowB, ybad, c0 * ob.nb, c1 * ob.nb);
+        k_oz_split_y<1><<<nsm_ * 4, 256, 0, s3>>>(Yd, ob, ozFrowB, ozYB, c0 * ob.nb, c1 * ob.nb);
+        CPF_CUDA_CHECK(cudaGetLastError());
+      }
+      CPF_CUDA_CHECK(cudaEventRecord(evEnd, s3));
+      CPF_CUDA_CHECK(cudaStreamWaitEvent(s, evEnd, 0));
+      cudaEventDestroy(ev);
+      cudaEventDestroy(evEnd);
+      Y = Yown;
+      oz_split(/*pass_b_done=*/true);
+      return true;
+    }
+  }
+  void oz_split(bool pass_b_done = false) {
     NvtxRange nvtx_("cpf.oz_split (int8 digit-plane images)");
     if (!use_oz || Jloc == 0) return;
     if constexpr (sizeof(T) == 8) {
       const double* Yd = reinterpret_cast<const double*>(Y);
       int* ybad = reinterpret_cast<int*>(red);  // scratch
-      CPF_CUDA_CHECK(cudaMemsetAsync(ybad, 0, sizeof(int), s));
+      if (!pass_b_done) CPF_CUDA_CHECK(cudaMemsetAsync(ybad, 0, sizeof(int), s));
       k_oz_rowexp<0><<<nsm_ * 8, 256, 0, s>>>(Yd, oa, ozFrowA, ybad);
-      k_oz_rowexp<1><<<nsm_ * 8, 256, 0, s>>>(Yd, ob, ozFrowB, ybad);
+      if (!pass_b_done) k_oz_rowexp<1><<<nsm_ * 8, 256, 0, s>>>(Yd, ob, ozFrowB, ybad);
       CPF_CUDA_CHECK(cudaGetLastError());
       int nbad = 0;
       CPF_CUDA_CHECK(cudaMemcpyAsync(&nbad, ybad, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -924,7 +962,7 @@ struct Engine final : EngineBase {
         return;
       }
       k_oz_split_y<0><<<nsm_ * 16, 256, 0, s>>>(Yd, oa, ozFrowA, ozYA);
-      k_oz_split_y<1><<<nsm_ * 16, 256, 0, s>>>(Yd, ob, ozFrowB, ozYB);
+      if (!pass_b_done) k_oz_split_y<1><<<nsm_ * 16, 256, 0, s>>>(Yd, ob, ozFrowB, ozYB);
       CPF_CUDA_CHECK(cudaGetLastError());
     }
   }
@@ -1917,6 +1955,11 @@ struct Engine final : EngineBase {
       Y = static_cast<const T*>(p);
     } else {
       if (!Yown) Yown = static_cast<T*>(big_alloc((size_t)std::max<int64_t>(Jloc, 1) * sizeof(T), false));
+      if (upload_with_split(p)) {
+        have_tensor = true;
+        ysq_cached = -1.0;
+        return;
+      }
       if (Jloc > 0) CPF_CUDA_CHECK(cudaMemcpyAsync(Yown, p, Jloc * sizeof(T), cudaMemcpyHostToDevice, s));
       Y = Yown;
     }

@@ -117,10 +117,12 @@ __device__ __forceinline__ bool oz_outside(double amax, double sumsq, int64_t K)
 // row exponents: thread per tile row (t, row); F = 0 for padding rows.  *ybad counts the rows
 // outside the accuracy envelope (cleared by the host before the launch).
 template <int MODE>
-__global__ void k_oz_rowexp(const double* __restrict__ Y, OzGeom g, int* __restrict__ Frow, int* __restrict__ ybad) {
+__global__ void k_oz_rowexp(const double* __restrict__ Y, OzGeom g, int* __restrict__ Frow, int* __restrict__ ybad,
+                            int64_t t0 = 0, int64_t t1 = -1) {
   pdl_wait();
   const int64_t K = MODE == 0 ? g.C : g.Lmid;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < g.ntiles * kOzM;
+  if (t1 < 0) t1 = g.ntiles;  // tiles [t0, t1): the whole image, or the part of it already uploaded
+  for (int64_t idx = t0 * kOzM + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < t1 * kOzM;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = idx / kOzM;
     const int row = (int)(idx - t * kOzM);
@@ -141,11 +143,13 @@ __global__ void k_oz_rowexp(const double* __restrict__ Y, OzGeom g, int* __restr
 // digit planes: work item = (tile, K block, K row k, quad of 4 i1) -> 8 x 4 bytes of the image
 template <int MODE>
 __global__ void k_oz_split_y(const double* __restrict__ Y, OzGeom g, const int* __restrict__ Frow,
-                             uint8_t* __restrict__ Yimg) {
+                             uint8_t* __restrict__ Yimg, int64_t t0 = 0, int64_t t1 = -1) {
   pdl_wait();
   const int64_t K = MODE == 0 ? g.C : g.Lmid;
-  const int64_t total = g.ntiles * g.nkb * (kOzK * kOzM / 4);
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+  if (t1 < 0) t1 = g.ntiles;
+  const int64_t per = g.nkb * (kOzK * kOzM / 4);  // work items per tile
+  const int64_t total = t1 * per;
+  for (int64_t idx = t0 * per + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int quad = (int)(idx & 31);
     const int k = (int)((idx >> 5) & 31);

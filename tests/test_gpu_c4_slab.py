@@ -51,3 +51,20 @@ def test_c4_slab_matches_reference_on_default_int8_path(api):
           f"factors rel = {fac_dev:.3e} (bound {FACTOR_RTOL:g})")
     assert fit_dev < FIT_ATOL
     assert fac_dev < FACTOR_RTOL
+
+
+@pytest.mark.slow
+def test_upload_with_split_gives_the_same_image(api, monkeypatch):
+    """fit() from host memory builds the pass-B digit-plane image behind the sliced upload
+    (Engine::upload_with_split); the result must be bit-identical to the one-copy path."""
+    from paper_1205_2584_b200 import synth
+
+    d = G.load_fit(NAME)
+    y = synth.make_tensor(G.synth_config(d), d["seed"])
+    conf = api.FitConfig(rank=d["rank"], variant=d["variant"], tau=d["tau"], tol=d["tol"],
+                         max_iters=8, seed=d["seed"], init="random")
+    res = api.fit(y, conf)
+    monkeypatch.setenv("CPF_UPLOAD_SPLIT", "0")
+    ref = api.fit(y, conf)
+    assert [(r.relerr, r.mu, r.accepted) for r in res.trace] == [(r.relerr, r.mu, r.accepted) for r in ref.trace]
+    assert np.array_equal(res.model.as_vector(), ref.model.as_vector())
