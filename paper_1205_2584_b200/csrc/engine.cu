@@ -907,8 +907,12 @@ struct Engine final : EngineBase {
   bool upload_with_split(const void* p) {
     if constexpr (sizeof(T) != 8) return false;
     else {
-      if (!use_oz || Cloc < 16 || Jloc < ((int64_t)1 << 27)) return false;
-      if (const char* e = knob("CPF_UPLOAD_SPLIT")) if (e[0] == '0') return false;
+      bool force = false;
+      if (const char* e = knob("CPF_UPLOAD_SPLIT")) {
+        if (e[0] == '0') return false;
+        force = true;  // tests: at any size
+      }
+      if (!use_oz || Cloc < 16 || (!force && Jloc < ((int64_t)1 << 27))) return false;
       const double* Yd = reinterpret_cast<const double*>(Yown);
       int* ybad = reinterpret_cast<int*>(red);  // scratch
       CPF_CUDA_CHECK(cudaMemsetAsync(ybad, 0, sizeof(int), s));

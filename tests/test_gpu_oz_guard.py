@@ -126,3 +126,31 @@ def test_guard_threshold_matches_documented_envelope():
         v = rng.standard_normal(k)
         assert np.max(np.abs(v)) / math.sqrt(np.mean(v * v)) < 16
     assert math.sqrt(257) > 16 >= math.sqrt(256)
+
+
+def test_spiky_tensor_rejected_after_sliced_upload(monkeypatch):
+    """The sliced host upload builds the pass-B image behind the slices (Engine::upload_with_split,
+    forced here at a small size); a tensor the guard then rejects must drop the images and still
+    fit on the fp64 passes like the oracle."""
+    import paper_1205_2584_b200 as api
+    from oracle import cp_oracle as O
+    from paper_1205_2584_b200 import _native
+
+    monkeypatch.setenv("CPF_UPLOAD_SPLIT", "1")
+    rng = np.random.default_rng(43)
+    y = 1e-3 * rng.standard_normal(DIMS)
+    y[:, :, 7] = 1.0
+    y = np.asfortranarray(y)
+    conf = api.FitConfig(rank=R, tau=1e-3, tol=0.0, max_iters=6, seed=5, init="random")
+    res = api.fit(y, conf)
+    assert res.pass_impl == _native.PASS_DMMA and res.tensor_guarded
+    ref = O.fit_lm(y, O.OracleConfig(rank=R, tau=1e-3, tol=0.0, max_iters=6, seed=5))
+    assert "".join("A" if t.accepted else "r" for t in res.trace) == ref.accepted
+    assert abs(res.final_relerr - ref.final_relerr) < 1e-10
+    # and an ordinary tensor through the same forced path keeps the int8 passes
+    y2 = np.asfortranarray(rng.standard_normal(DIMS))
+    res2 = api.fit(y2, conf)
+    ref2 = O.fit_lm(y2, O.OracleConfig(rank=R, tau=1e-3, tol=0.0, max_iters=6, seed=5))
+    assert res2.pass_impl == _native.PASS_OZAKI and not res2.tensor_guarded
+    assert "".join("A" if t.accepted else "r" for t in res2.trace) == ref2.accepted
+    assert abs(res2.final_relerr - ref2.final_relerr) < 1e-10
