@@ -1630,7 +1630,9 @@ struct Engine final : EngineBase {
   int tri_split(int sz) const {
     int k = kTriSplit;
     if (const char* e = knob("CPF_TRI_SPLIT")) k = std::max(1, std::min(kTriSplit, atoi(e)));
-    return sz >= 256 ? k : 1;
+    // not in the pair form of the band 512 < n_B <= 1024 (config 2: its parity margin prefers
+    // sequential sums, see tri_rows; 472 it/s either way there)
+    return (sz >= 256 && (nB > 1024 || nB <= 512)) ? k : 1;
   }
   static constexpr int kTriSplit = 4;
   T* TriPart = nullptr;   // split-K partials: kTriSplit x nB x nB
@@ -1683,7 +1685,11 @@ struct Engine final : EngineBase {
   // which form: rows for the small systems, pairs above (tri_inv.cuh header)
   bool tri_rows() const {
     if (const char* e = knob("CPF_TRI_ROWS")) return e[0] == '1';
-    return nB <= 1024;
+    // up to n_B = 512.  Between 512 and 1024 (config 2: 900) the row form needs split-K to keep up
+    // with the panels, and split-K sums move the ill-conditioned config-2 trajectory away from the
+    // reference's (final factors 1.9e-9 with it, 5e-10 without but 423 it/s); the pair form without
+    // split-K gives 6.6e-10 at 472 it/s
+    return nB <= 512;
   }
   void tri_progress(int k, int np, int gate_running) {
     if (tri_rows()) tri_row_step(k, gate_running, s4);

@@ -14,9 +14,10 @@ FIT_ATOL = 1e-10
 # Configs 1 and 2 are ill-conditioned enough that the reference's OWN factors move by 7e-8-1.1e-7
 # (C1) and 1e-10-4e-10 (C2) under rounding-level changes (profiles/r01_parity_sensitivity.txt,
 # tools/parity_sensitivity.py).  Measured engine distances (profiles/r02_parity_margins.txt): C1
-# 4.3e-8, C2 6.6e-10; the bounds keep a >= 2x margin over them and stay at the reference's own
-# sensitivity.
-FACTOR_RTOL_BY_CONFIG = {"fit_c1_s0_auto": 1e-7, "fit_c2_s0_auto": 2e-9}
+# 3.9e-8, C2 6.6e-10.  C2 meets the north-star 1e-9 like every other config; only C1 keeps a bound
+# at the reference's own sensitivity.  (C2 is why the triangular inverse does not split K for
+# n_B <= 1024: with split-K partial sums the same fit lands 1.9e-9 from the reference.)
+FACTOR_RTOL_BY_CONFIG = {"fit_c1_s0_auto": 1e-7}
 
 
 def _rel(a, b):
